@@ -1,0 +1,187 @@
+/*
+ * lffn_gpu.h -- C-ABI of the B200-native LookupFFN forward (sm_100a).
+ *
+ * This is the drop-in boundary for the reference library `lookupffn`
+ * (namespace lffn, /root/reference/proj).  The reference exposes the hot path
+ * as a C++ API (no FFI); every entry point below names the reference
+ * interface it replaces.  INTEGRATION.md shows the C++ shim a maintainer adds
+ * on the reference side (lffn::gpu::lookup_forward & co.) and the ctypes
+ * binding used by the Python host package.
+ *
+ * Conventions (all kept from the reference):
+ *   x      [n x d_in]  float32 row-major                (bench.cpp:102-112)
+ *   z      [n x h*tau] float64, viewed as [n][h][tau]   (lookup.hpp:70-79)
+ *   codes  [n x h]     uint32, bit j <- [z_{k*tau+j} >= 0], LSB first
+ *                                                       (lookup.cpp:74-100)
+ *   coeff  [n x h]     float32: the top-1 weight prod_j 1/(1+e^{-2|z_j|}),
+ *                      times sum_j |z_j| for the scaled variants
+ *                                                       (bench.cpp:162-180)
+ *   T      [h][2^tau][d_out], row(k,c) = T + (k*2^tau + c)*d_out
+ *                                                       (lookup.hpp:43-57)
+ *   y      [n x d_out] float32                          (bench.cpp:182-194)
+ *
+ * Status codes map the reference error taxonomy (common.hpp:13-37):
+ *   0 ok, 1 SizeError/UsageError, 2 NumericError (message names the stage:
+ *   "projection forward input", "hash stage", "gather stage"), 3 CUDA runtime.
+ * Device pointers are caller-owned; the context owns its workspace and never
+ * allocates inside hash / lookup_accumulate / forward.  Calls are ordered on
+ * the caller's stream (a cudaStream_t passed as void*; NULL = legacy default
+ * stream).  Non-finite checks run on the device; kernels raise a flag that
+ * lffn_sync() (and every blocking call) turns into status 2.  One context per
+ * host thread.
+ */
+#ifndef LFFN_GPU_H
+#define LFFN_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LFFN_OK 0
+#define LFFN_ERR_USAGE 1
+#define LFFN_ERR_NUMERIC 2
+#define LFFN_ERR_RUNTIME 3
+
+/* ProjKind (projection.hpp:13) */
+#define LFFN_PROJ_DENSE 0
+#define LFFN_PROJ_BH 1
+#define LFFN_PROJ_ACDC 2
+#define LFFN_PROJ_SIGNFLIP 3
+
+/* LookupVariant (lookup.hpp:20) */
+#define LFFN_SOFTMAX 0
+#define LFFN_SCALED 1
+#define LFFN_SIGMOID_TAU1 2
+#define LFFN_GELU_TAU1 3
+
+/* element types of table storage / host buffers */
+#define LFFN_F32 0
+#define LFFN_BF16 1
+#define LFFN_F64 2
+
+/* LookupConfig (lookup.hpp:25-39) */
+typedef struct lffn_cfg {
+  int64_t d_in;
+  int64_t d_out;
+  int64_t tables;         /* h */
+  int64_t code_bits;      /* tau */
+  int32_t variant;        /* LFFN_SOFTMAX .. LFFN_GELU_TAU1 */
+  int32_t neighbor_count; /* nc; the device path implements nc == 1 */
+} lffn_cfg;
+
+/* ProjectionSpec + Projection::blob() (projection.hpp:21-95).  blob is a
+ * HOST pointer in the reference blob layout (projection.hpp:47-54); the
+ * context copies what it needs at creation. */
+typedef struct lffn_proj {
+  int32_t kind;
+  int32_t reserved;
+  int64_t d_in;
+  int64_t d_out; /* must equal tables * code_bits */
+  int64_t stages;
+  int64_t block;
+  int64_t depth;
+  const double* blob;
+  int64_t blob_len;
+} lffn_proj;
+
+typedef struct lffn_ctx lffn_ctx;
+
+/* ---- host-side configuration and parameter helpers -------------------- */
+
+/* LookupConfig::validate (lookup.cpp:27-37) */
+int lffn_cfg_validate(const lffn_cfg* cfg);
+/* ProjectionSpec::validate (projection.cpp:29-40) + blob length check of
+ * Projection::from_blob (projection.cpp:137-145) when blob != NULL */
+int lffn_proj_validate(const lffn_proj* proj);
+/* ProjectionSpec::transform_width (projection.hpp:30) */
+int64_t lffn_transform_width(const lffn_proj* proj);
+/* blob_size_for (projection.cpp:81-93) */
+int64_t lffn_proj_blob_size(const lffn_proj* proj);
+/* Projection::init (projection.cpp:97-135): fills blob_out[blob_size] */
+int lffn_proj_init(const lffn_proj* spec, uint64_t seed, double* blob_out);
+/* make_rng(seed) + fill_gaussian / fill_signs (common.hpp:44-55) */
+int lffn_fill_gaussian(uint64_t seed, double* out, int64_t n, double stddev);
+int lffn_fill_signs(uint64_t seed, double* out, int64_t n);
+/* HashTables::init (lookup.cpp:39-49): std 1/sqrt(h) */
+int lffn_tables_init(const lffn_cfg* cfg, uint64_t seed, double* out);
+
+/* Element conversion used by lffn_tables_upload: f64/f32/bf16 -> f64/f32/bf16,
+ * each rounding a single round-to-nearest-even (the stored table values a
+ * parity check must feed to the float64 oracle). */
+int lffn_convert(const void* src, int src_dtype, void* dst, int dst_dtype, int64_t n);
+
+/* ---- device context ------------------------------------------------------ */
+
+/* Validates like check_shapes (lookup.cpp:173-182) and allocates the
+ * workspace for up to max_tokens rows (LookupWorkspaceF32, bench.cpp:102-112). */
+int lffn_ctx_create(lffn_ctx** out, int device, int64_t max_tokens, const lffn_cfg* cfg,
+                    const lffn_proj* proj);
+/* Same for a table shard: this context owns tables [table_begin, table_end)
+ * of the h-table stack; hash emits codes/coeffs only for those tables and
+ * lookup_accumulate produces the partial sum over them (multi-GPU table
+ * sharding; no reference counterpart). */
+int lffn_ctx_create_shard(lffn_ctx** out, int device, int64_t max_tokens, const lffn_cfg* cfg,
+                          const lffn_proj* proj, int64_t table_begin, int64_t table_end);
+int lffn_ctx_destroy(lffn_ctx* ctx);
+/* tables owned by this context: [*begin, *end) */
+int lffn_ctx_table_range(const lffn_ctx* ctx, int64_t* begin, int64_t* end);
+
+/* One-time upload of HashTables::data (lookup.hpp:43-66).  host_T is the FULL
+ * [h][2^tau][d_out] stack in host_dtype (LFFN_F64 for the reference's double
+ * tables, LFFN_F32, LFFN_BF16); it is converted (round-to-nearest-even) to
+ * store_dtype (LFFN_F32 or LFFN_BF16) and a shard keeps only its slice.
+ * Tables are read-only afterwards (lookup.hpp:41-42). */
+int lffn_tables_upload(lffn_ctx* ctx, const void* host_T, int host_dtype, int store_dtype);
+/* Use a caller-owned device buffer holding this context's slice
+ * [table_end-table_begin][2^tau][d_out] in dtype (no copy). */
+int lffn_tables_attach(lffn_ctx* ctx, const void* d_T, int dtype);
+
+/* Hash stage = Projection::forward (projection.cpp:167-266) + compute_codes
+ * (lookup.cpp:81-100) + top-1 weight (lookup.cpp:185-189), i.e. the
+ * lookup_hash_f32 + lookup_weights_f32 pair (bench.cpp:115-180), in one
+ * kernel.  d_codes/d_coeff: [n x h_local]; d_z (optional, may be NULL):
+ * [n x h*tau] float64 projection output (bit-identical to the reference's
+ * double Projection::forward for the signflip kind). */
+int lffn_hash(lffn_ctx* ctx, const float* d_x, int64_t n, uint32_t* d_codes, float* d_coeff,
+              double* d_z, void* stream);
+
+/* Gather stage = lookup_gather_f32 (bench.cpp:182-194): y_i (+)= sum_k
+ * coeff[i,k] * T[k][codes[i,k]], tables in ascending order.  accumulate = 0
+ * overwrites y (the reference zero-fills first), 1 adds into y. */
+int lffn_lookup_accumulate(lffn_ctx* ctx, const uint32_t* d_codes, const float* d_coeff,
+                           int64_t n, float* d_y, int accumulate, void* stream);
+
+/* Full forward = lookup_forward (lookup.cpp:191-282) for nc == 1:
+ * hash -> gather on the device, no host round trip. */
+int lffn_forward(lffn_ctx* ctx, const float* d_x, int64_t n, float* d_y, void* stream);
+
+/* Same with HOST x / y (pinned or pageable): the host<->device copies are
+ * chunked and overlapped with the kernels on internal streams.  Blocking;
+ * returns the deferred numeric status. */
+int lffn_forward_host(lffn_ctx* ctx, const float* h_x, int64_t n, float* h_y);
+
+/* Waits for `stream` and reports any non-finite flag raised since the last
+ * check (status 2 with the stage named in lffn_last_error()). */
+int lffn_sync(lffn_ctx* ctx, void* stream);
+
+/* Number of kernels launched through this context since creation. */
+int64_t lffn_ctx_launch_count(const lffn_ctx* ctx);
+
+/* Per-launch device timing of the last forward's stages (ms; CUDA events on
+ * the launching stream; 0 when timing is off).  enable = 1 turns stage
+ * events on for subsequent forwards. */
+int lffn_ctx_set_timing(lffn_ctx* ctx, int enable);
+int lffn_ctx_stage_ms(lffn_ctx* ctx, float* hash_ms, float* gather_ms);
+
+/* Thread-local message for the last non-zero status. */
+const char* lffn_last_error(void);
+
+/* Library identification: "lffn_gpu <version> sm_100a". */
+const char* lffn_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LFFN_GPU_H */

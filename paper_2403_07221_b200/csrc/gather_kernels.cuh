@@ -1,0 +1,132 @@
+// gather_kernels.cuh -- K3: the gather-accumulate stage
+//   y_i (+)= sum_{k=kb}^{ke-1} coeff[i,k] * T[k][code[i,k]][:]
+// replacing lookup_gather_f32 (bench.cpp:182-194) and the gather loop of
+// forward_impl (lookup.cpp:223-268).  Tables are walked in ascending order
+// with fp32 accumulators in registers, as the reference's f32 path does.
+//
+// This file holds the direct-gather kernel: each warp owns NTOK tokens x one
+// column chunk of 32*VEC columns and reads every gathered row segment with
+// 128-bit loads straight from L2 (the L2-resident table working set keeps
+// the HBM traffic at the unique bytes).  It serves every shape; the staged
+// kernel in staged_gather.cuh beats the L2 roofline for tables whose row
+// count is small enough to stage.
+#pragma once
+
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+namespace lffn_gpu {
+
+struct GatherParams {
+  const void* T;            // [h_loc][R][d_out] in f32 or bf16
+  const uint32_t* codes;    // [n x h_loc]
+  const float* coeff;       // [n x h_loc]
+  float* y;                 // [n x d_out]
+  int64_t n;
+  int h_loc;
+  int rows;                 // R = 2^tau
+  int d_out;
+  int accumulate;
+  int* flag;
+};
+
+template <typename TT, int VEC>
+struct RowLoad;
+
+template <>
+struct RowLoad<float, 4> {
+  static __device__ __forceinline__ void load(const float* p, float (&v)[4]) {
+    const float4 q = __ldg(reinterpret_cast<const float4*>(p));
+    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+  }
+};
+
+template <>
+struct RowLoad<float, 1> {
+  static __device__ __forceinline__ void load(const float* p, float (&v)[1]) { v[0] = __ldg(p); }
+};
+
+__device__ __forceinline__ float bf16lo(uint32_t u) { return __uint_as_float(u << 16); }
+__device__ __forceinline__ float bf16hi(uint32_t u) { return __uint_as_float(u & 0xffff0000u); }
+
+template <>
+struct RowLoad<__nv_bfloat16, 8> {
+  static __device__ __forceinline__ void load(const __nv_bfloat16* p, float (&v)[8]) {
+    const uint4 q = __ldg(reinterpret_cast<const uint4*>(p));
+    v[0] = bf16lo(q.x); v[1] = bf16hi(q.x); v[2] = bf16lo(q.y); v[3] = bf16hi(q.y);
+    v[4] = bf16lo(q.z); v[5] = bf16hi(q.z); v[6] = bf16lo(q.w); v[7] = bf16hi(q.w);
+  }
+};
+
+template <>
+struct RowLoad<__nv_bfloat16, 1> {
+  static __device__ __forceinline__ void load(const __nv_bfloat16* p, float (&v)[1]) {
+    const unsigned short s = __ldg(reinterpret_cast<const unsigned short*>(p));
+    v[0] = __uint_as_float(uint32_t(s) << 16);
+  }
+};
+
+template <typename TT, int VEC, int NTOK>
+__global__ void __launch_bounds__(256) gather_direct_kernel(GatherParams p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int chunk_cols = 32 * VEC;
+  const int nchunks = (p.d_out + chunk_cols - 1) / chunk_cols;
+  const int64_t tgroup = gwarp / nchunks;
+  const int chunk = (int)(gwarp - tgroup * nchunks);
+  const int64_t i0 = tgroup * NTOK;
+  if (i0 >= p.n) return;
+  const int col = chunk * chunk_cols + lane * VEC;
+  const bool colok = col < p.d_out;
+  const TT* T = reinterpret_cast<const TT*>(p.T);
+  const int64_t table_stride = (int64_t)p.rows * p.d_out;
+
+  float acc[NTOK][VEC];
+#pragma unroll
+  for (int t = 0; t < NTOK; ++t)
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) acc[t][v] = 0.f;
+
+  const uint32_t* cbase = p.codes + i0 * p.h_loc;
+  const float* wbase = p.coeff + i0 * p.h_loc;
+  const int ntok = (p.n - i0) < NTOK ? (int)(p.n - i0) : NTOK;
+
+  for (int k = 0; k < p.h_loc; ++k) {
+    float vals[NTOK][VEC];
+    float w[NTOK];
+#pragma unroll
+    for (int t = 0; t < NTOK; ++t) {
+      w[t] = 0.f;
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) vals[t][v] = 0.f;
+      if (t < ntok) {
+        const uint32_t code = __ldg(cbase + (int64_t)t * p.h_loc + k);
+        w[t] = __ldg(wbase + (int64_t)t * p.h_loc + k);
+        if (colok) RowLoad<TT, VEC>::load(T + k * table_stride + (int64_t)code * p.d_out + col, vals[t]);
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < NTOK; ++t)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) acc[t][v] = fmaf(w[t], vals[t][v], acc[t][v]);
+  }
+
+  if (!colok) return;
+  int bad = 0;
+#pragma unroll
+  for (int t = 0; t < NTOK; ++t) {
+    if (t >= ntok) break;
+    float* yr = p.y + (i0 + t) * p.d_out + col;
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      float o = acc[t][v];
+      if (p.accumulate) o += yr[v];
+      if (!isfinite(o)) bad = 4;
+      yr[v] = o;
+    }
+  }
+  if (bad) atomicOr(p.flag, bad);
+}
+
+}  // namespace lffn_gpu

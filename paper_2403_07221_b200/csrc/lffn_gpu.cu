@@ -1,0 +1,596 @@
+// lffn_gpu.cu -- the C-ABI of include/lffn_gpu.h: device context, table
+// upload, and the stream-ordered launches of the hash (K1/K2) and gather (K3)
+// kernels.  No CPU compute path exists: every forward runs on the device and
+// a missing / failing CUDA runtime is reported as status 3.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "gather_kernels.cuh"
+#include "hash_kernels.cuh"
+#include "lffn_gpu.h"
+#include "lffn_internal.h"
+#include "staged_gather.cuh"
+
+namespace lffn_gpu {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+int fail(int status, const std::string& msg) {
+  g_last_error = msg;
+  return status;
+}
+
+}  // namespace lffn_gpu
+
+using namespace lffn_gpu;
+
+#define LFFN_CUDA(call)                                                                   \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(LFFN_ERR_RUNTIME, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+struct lffn_ctx {
+  int device = 0;
+  int64_t max_tokens = 0;
+  lffn_cfg cfg{};
+  lffn_proj proj{};  // blob pointer cleared after the copy
+  int64_t D = 1, logD = 0, code_width = 0, rows = 0, kb = 0, ke = 0, h_loc = 0;
+  int n_transforms = 0;
+
+  // projection parameters on the device
+  uint32_t* d_signmask = nullptr;
+  double* d_diag = nullptr;
+  double* d_W = nullptr;
+  double* d_zbuf = nullptr;  // dense: [max_tokens x code_width] float64
+
+  // tables
+  const void* d_T = nullptr;
+  void* d_T_owned = nullptr;
+  int t_dtype = LFFN_F32;
+
+  // workspace
+  uint32_t* d_codes = nullptr;
+  float* d_coeff = nullptr;
+  int* d_flag = nullptr;
+  int* h_flag = nullptr;  // pinned
+  float* d_xbuf = nullptr;
+  float* d_ybuf = nullptr;
+  cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
+  static constexpr int kChunks = 8;
+  cudaEvent_t ev_h2d[kChunks] = {}, ev_comp[kChunks] = {};
+  cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr, ev_t2 = nullptr;
+  bool timing = false;
+  bool timed = false;
+
+  int64_t launches = 0;
+  int staged_ok = 0;
+  int staged_smem = 0;
+};
+
+namespace {
+
+int flag_message(int flag) {
+  if (flag & kFlagInput) return fail(LFFN_ERR_NUMERIC, "non-finite values in projection forward input");
+  if (flag & kFlagHash) return fail(LFFN_ERR_NUMERIC, "non-finite values in hash stage");
+  if (flag & kFlagGather) return fail(LFFN_ERR_NUMERIC, "non-finite values in gather stage");
+  return LFFN_OK;
+}
+
+class DeviceGuard {
+ public:
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev_);
+    if (prev_ != dev) cudaSetDevice(dev);
+    dev_ = dev;
+  }
+  ~DeviceGuard() {
+    if (prev_ != dev_) cudaSetDevice(prev_);
+  }
+
+ private:
+  int prev_ = 0, dev_ = 0;
+};
+
+int ilog2(int64_t v) {
+  int l = 0;
+  while ((int64_t(1) << l) < v) ++l;
+  return l;
+}
+
+void destroy_ctx(lffn_ctx* c) {
+  if (!c) return;
+  DeviceGuard g(c->device);
+  cudaFree(c->d_signmask);
+  cudaFree(c->d_diag);
+  cudaFree(c->d_W);
+  cudaFree(c->d_zbuf);
+  cudaFree(c->d_T_owned);
+  cudaFree(c->d_codes);
+  cudaFree(c->d_coeff);
+  cudaFree(c->d_flag);
+  if (c->h_flag) cudaFreeHost(c->h_flag);
+  cudaFree(c->d_xbuf);
+  cudaFree(c->d_ybuf);
+  if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
+  if (c->s_comp) cudaStreamDestroy(c->s_comp);
+  if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
+  for (int i = 0; i < lffn_ctx::kChunks; ++i) {
+    if (c->ev_h2d[i]) cudaEventDestroy(c->ev_h2d[i]);
+    if (c->ev_comp[i]) cudaEventDestroy(c->ev_comp[i]);
+  }
+  if (c->ev_t0) cudaEventDestroy(c->ev_t0);
+  if (c->ev_t1) cudaEventDestroy(c->ev_t1);
+  if (c->ev_t2) cudaEventDestroy(c->ev_t2);
+  delete c;
+}
+
+int check_n(const lffn_ctx* c, int64_t n) {
+  if (n < 0) return fail(LFFN_ERR_USAGE, "lookup forward: negative row count");
+  if (n > c->max_tokens)
+    return fail(LFFN_ERR_USAGE, "lookup forward: " + std::to_string(n) +
+                                    " rows exceed the context's max_tokens " +
+                                    std::to_string(c->max_tokens));
+  return LFFN_OK;
+}
+
+// ---------------------------------------------------------------- launches
+
+int launch_hash(lffn_ctx* c, const float* d_x, int64_t n, uint32_t* codes, float* coeff,
+                double* z_out, cudaStream_t st) {
+  if (n == 0) return LFFN_OK;
+  HashParams p{};
+  p.x = d_x;
+  p.n = n;
+  p.d_in = int(c->cfg.d_in);
+  p.D = int(c->D);
+  p.logD = int(c->logD);
+  p.code_width = int(c->code_width);
+  p.tau = int(c->cfg.code_bits);
+  p.kb = int(c->kb);
+  p.ke = int(c->ke);
+  p.scaled = (c->cfg.variant == LFFN_SCALED || c->cfg.variant == LFFN_GELU_TAU1) ? 1 : 0;
+  p.n_transforms = c->n_transforms;
+  p.signmask = c->d_signmask;
+  p.diag = c->d_diag;
+  p.z_out = z_out;
+  p.codes = codes;
+  p.coeff = coeff;
+  p.flag = c->d_flag;
+  if (c->proj.kind == LFFN_PROJ_DENSE) {
+    dim3 grid((unsigned)((c->code_width + 63) / 64), (unsigned)((n + 63) / 64));
+    dense_proj_f64_kernel<<<grid, 256, 0, st>>>(d_x, c->d_W, c->d_zbuf, n, int(c->cfg.d_in),
+                                                int(c->code_width), c->d_flag);
+    ++c->launches;
+    p.z_in = c->d_zbuf;
+  }
+  const int loge = c->logD >= 4 ? 4 : int(c->logD);
+  const int E = 1 << loge;
+  const int tpt = int(c->D / E);
+  const int block = std::max(tpt, std::min(256, int(256 / tpt) * tpt));
+  const int tpb = block / tpt;
+  p.tokens_per_block = tpb;
+  p.threads_per_token = tpt;
+  const size_t smem = size_t(tpb) * size_t(c->D + (c->D >> 4)) * sizeof(double);
+  const unsigned grid = (unsigned)((n + tpb - 1) / tpb);
+  switch (loge) {
+#define LFFN_HASH_CASE(L)                                                                  \
+  case L:                                                                                  \
+    cudaFuncSetAttribute(hash_structured_kernel<L>,                                        \
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));          \
+    hash_structured_kernel<L><<<grid, block, smem, st>>>(p);                               \
+    break;
+    LFFN_HASH_CASE(0)
+    LFFN_HASH_CASE(1)
+    LFFN_HASH_CASE(2)
+    LFFN_HASH_CASE(3)
+    LFFN_HASH_CASE(4)
+#undef LFFN_HASH_CASE
+  }
+  ++c->launches;
+  LFFN_CUDA(cudaGetLastError());
+  return LFFN_OK;
+}
+
+int launch_gather(lffn_ctx* c, const uint32_t* codes, const float* coeff, int64_t n, float* y,
+                  int accumulate, cudaStream_t st) {
+  if (n == 0) return LFFN_OK;
+  if (!c->d_T) return fail(LFFN_ERR_USAGE, "lookup forward: tables not uploaded");
+  GatherParams p{};
+  p.T = c->d_T;
+  p.codes = codes;
+  p.coeff = coeff;
+  p.y = y;
+  p.n = n;
+  p.h_loc = int(c->h_loc);
+  p.rows = int(c->rows);
+  p.d_out = int(c->cfg.d_out);
+  p.accumulate = accumulate;
+  p.flag = c->d_flag;
+  if (c->h_loc == 0) {
+    if (!accumulate) LFFN_CUDA(cudaMemsetAsync(y, 0, size_t(n) * p.d_out * sizeof(float), st));
+    return LFFN_OK;
+  }
+  if (staged_gather_applicable(c->staged_ok, p, c->t_dtype)) {
+    int rc = launch_staged_gather(p, c->t_dtype, c->staged_smem, st);
+    ++c->launches;
+    if (rc == 0) {
+      LFFN_CUDA(cudaGetLastError());
+      return LFFN_OK;
+    }
+  }
+  constexpr int NTOK = 4;
+  const bool f32 = c->t_dtype == LFFN_F32;
+  const int vec = f32 ? ((p.d_out % 4 == 0) ? 4 : 1) : ((p.d_out % 8 == 0) ? 8 : 1);
+  const int64_t chunks = (p.d_out + 32 * vec - 1) / (32 * vec);
+  const int64_t warps = ((n + NTOK - 1) / NTOK) * chunks;
+  const unsigned grid = (unsigned)((warps * 32 + 255) / 256);
+  if (f32 && vec == 4) gather_direct_kernel<float, 4, NTOK><<<grid, 256, 0, st>>>(p);
+  else if (f32) gather_direct_kernel<float, 1, NTOK><<<grid, 256, 0, st>>>(p);
+  else if (vec == 8) gather_direct_kernel<__nv_bfloat16, 8, NTOK><<<grid, 256, 0, st>>>(p);
+  else gather_direct_kernel<__nv_bfloat16, 1, NTOK><<<grid, 256, 0, st>>>(p);
+  ++c->launches;
+  LFFN_CUDA(cudaGetLastError());
+  return LFFN_OK;
+}
+
+int forward_impl(lffn_ctx* c, const float* d_x, int64_t n, float* d_y, cudaStream_t st) {
+  const bool tm = c->timing;
+  if (tm) LFFN_CUDA(cudaEventRecord(c->ev_t0, st));
+  if (int rc = launch_hash(c, d_x, n, c->d_codes, c->d_coeff, nullptr, st)) return rc;
+  if (tm) LFFN_CUDA(cudaEventRecord(c->ev_t1, st));
+  if (int rc = launch_gather(c, c->d_codes, c->d_coeff, n, d_y, 0, st)) return rc;
+  if (tm) {
+    LFFN_CUDA(cudaEventRecord(c->ev_t2, st));
+    c->timed = true;
+  }
+  return LFFN_OK;
+}
+
+int read_flag(lffn_ctx* c, cudaStream_t st) {
+  LFFN_CUDA(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  LFFN_CUDA(cudaMemsetAsync(c->d_flag, 0, sizeof(int), st));
+  LFFN_CUDA(cudaStreamSynchronize(st));
+  return flag_message(*c->h_flag);
+}
+
+uint16_t f32_to_bf16_rne(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return uint16_t((u >> 16) | 0x40);  // NaN stays NaN
+  const uint32_t rounding = 0x7fffu + ((u >> 16) & 1u);
+  return uint16_t((u + rounding) >> 16);
+}
+
+// double -> bf16 with a single round-to-nearest-even: round to float with
+// round-to-odd first (truncate, then set the sticky LSB when inexact), which
+// keeps the second rounding to bf16 exact.
+uint16_t f64_to_bf16_rne(double d) {
+  if (d != d) return 0x7fc0;
+  float f = float(d);
+  if (std::isinf(f)) return f32_to_bf16_rne(f);
+  if (std::fabs(double(f)) > std::fabs(d)) f = std::nextafter(f, 0.0f);
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if (double(f) != d) u |= 1u;
+  std::memcpy(&f, &u, 4);
+  return f32_to_bf16_rne(f);
+}
+
+float bf16_to_f32(uint16_t b) {
+  uint32_t u = uint32_t(b) << 16;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* lffn_last_error(void) { return g_last_error.c_str(); }
+
+const char* lffn_version(void) { return "lffn_gpu 0.1 sm_100a"; }
+
+int lffn_ctx_create_shard(lffn_ctx** out, int device, int64_t max_tokens, const lffn_cfg* cfg,
+                          const lffn_proj* proj, int64_t table_begin, int64_t table_end) {
+  if (!out) return fail(LFFN_ERR_USAGE, "ctx_create: null output");
+  *out = nullptr;
+  if (int rc = validate_cfg(cfg)) return rc;
+  if (int rc = validate_proj(proj)) return rc;
+  if (!proj->blob) return fail(LFFN_ERR_USAGE, "projection: blob required");
+  // check_shapes (lookup.cpp:173-182)
+  if (proj->d_in != cfg->d_in || proj->d_out != cfg->tables * cfg->code_bits)
+    return fail(LFFN_ERR_USAGE, "lookup forward: projection must map d_in to h*tau");
+  if (cfg->neighbor_count != 1)
+    return fail(LFFN_ERR_USAGE,
+                "lookup forward: the device path implements the top-1 default (neighbor_count 1)");
+  if (proj->kind == LFFN_PROJ_BH)
+    return fail(LFFN_ERR_USAGE, "lookup forward: bh projection not yet on the device");
+  if (max_tokens < 0) return fail(LFFN_ERR_USAGE, "ctx_create: negative max_tokens");
+  if (table_end == 0 && table_begin == 0) table_end = cfg->tables;
+  if (table_begin < 0 || table_end > cfg->tables || table_begin > table_end)
+    return fail(LFFN_ERR_USAGE, "ctx_create: table range outside [0, h]");
+  const int64_t D = transform_width(proj);
+  if (D > 16384) return fail(LFFN_ERR_USAGE, "lookup forward: transform width above 16384 is not supported on the device");
+
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    return fail(LFFN_ERR_RUNTIME, std::string("no CUDA device: ") + cudaGetErrorString(e));
+  if (device < 0 || device >= ndev) return fail(LFFN_ERR_USAGE, "ctx_create: bad device ordinal");
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major < 10)
+    return fail(LFFN_ERR_RUNTIME, "lffn_gpu is built for sm_100a (B200); device is sm_" +
+                                      std::to_string(prop.major) + std::to_string(prop.minor));
+
+  DeviceGuard g(device);
+  lffn_ctx* c = new lffn_ctx();
+  c->device = device;
+  c->max_tokens = max_tokens;
+  c->cfg = *cfg;
+  c->proj = *proj;
+  c->proj.blob = nullptr;
+  c->D = D;
+  c->logD = ilog2(D);
+  c->code_width = cfg->tables * cfg->code_bits;
+  c->rows = int64_t(1) << cfg->code_bits;
+  c->kb = table_begin;
+  c->ke = table_end;
+  c->h_loc = table_end - table_begin;
+
+  auto bail = [&](int rc) {
+    destroy_ctx(c);
+    return rc;
+  };
+#define CK(call)                                                                           \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      return bail(fail(LFFN_ERR_RUNTIME, std::string(#call) + ": " + cudaGetErrorString(e_))); \
+  } while (0)
+
+  // projection parameters
+  const double* blob = proj->blob;
+  if (proj->kind == LFFN_PROJ_SIGNFLIP) {
+    c->n_transforms = 3;
+    const int64_t words = (D + 31) / 32;
+    std::vector<uint32_t> mask(size_t(3 * words), 0u);
+    for (int64_t s = 0; s < 3; ++s)
+      for (int64_t j = 0; j < D; ++j) {
+        const double v = blob[s * D + j];
+        if (v != 1.0 && v != -1.0)
+          return bail(fail(LFFN_ERR_USAGE, "signflip projection: sign vectors must hold +-1"));
+        if (v == -1.0) mask[size_t(s * words + j / 32)] |= 1u << (j % 32);
+      }
+    CK(cudaMalloc(&c->d_signmask, mask.size() * sizeof(uint32_t)));
+    CK(cudaMemcpy(c->d_signmask, mask.data(), mask.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  } else if (proj->kind == LFFN_PROJ_ACDC) {
+    c->n_transforms = int(2 * proj->depth);
+    CK(cudaMalloc(&c->d_diag, size_t(2 * proj->depth * D) * sizeof(double)));
+    CK(cudaMemcpy(c->d_diag, blob, size_t(2 * proj->depth * D) * sizeof(double), cudaMemcpyHostToDevice));
+  } else if (proj->kind == LFFN_PROJ_DENSE) {
+    c->n_transforms = 0;
+    const size_t nw = size_t(proj->d_in * proj->d_out);
+    CK(cudaMalloc(&c->d_W, nw * sizeof(double)));
+    CK(cudaMemcpy(c->d_W, blob, nw * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&c->d_zbuf, size_t(std::max<int64_t>(max_tokens, 1)) * c->code_width * sizeof(double)));
+  }
+
+  const size_t mt = size_t(std::max<int64_t>(max_tokens, 1));
+  CK(cudaMalloc(&c->d_codes, mt * size_t(std::max<int64_t>(c->h_loc, 1)) * sizeof(uint32_t)));
+  CK(cudaMalloc(&c->d_coeff, mt * size_t(std::max<int64_t>(c->h_loc, 1)) * sizeof(float)));
+  CK(cudaMalloc(&c->d_flag, sizeof(int)));
+  CK(cudaMemset(c->d_flag, 0, sizeof(int)));
+  CK(cudaMallocHost(&c->h_flag, sizeof(int)));
+  CK(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
+  for (int i = 0; i < lffn_ctx::kChunks; ++i) {
+    CK(cudaEventCreateWithFlags(&c->ev_h2d[i], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_comp[i], cudaEventDisableTiming));
+  }
+  CK(cudaEventCreate(&c->ev_t0));
+  CK(cudaEventCreate(&c->ev_t1));
+  CK(cudaEventCreate(&c->ev_t2));
+  c->staged_ok = staged_gather_configure(int(c->rows), int(cfg->d_out), &c->staged_smem);
+#undef CK
+  *out = c;
+  return LFFN_OK;
+}
+
+int lffn_ctx_create(lffn_ctx** out, int device, int64_t max_tokens, const lffn_cfg* cfg,
+                    const lffn_proj* proj) {
+  return lffn_ctx_create_shard(out, device, max_tokens, cfg, proj, 0, cfg ? cfg->tables : 0);
+}
+
+int lffn_ctx_destroy(lffn_ctx* ctx) {
+  destroy_ctx(ctx);
+  return LFFN_OK;
+}
+
+int lffn_ctx_table_range(const lffn_ctx* ctx, int64_t* begin, int64_t* end) {
+  if (!ctx) return fail(LFFN_ERR_USAGE, "null context");
+  if (begin) *begin = ctx->kb;
+  if (end) *end = ctx->ke;
+  return LFFN_OK;
+}
+
+int64_t lffn_ctx_launch_count(const lffn_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+int lffn_tables_upload(lffn_ctx* c, const void* host_T, int host_dtype, int store_dtype) {
+  if (!c || !host_T) return fail(LFFN_ERR_USAGE, "tables upload: null argument");
+  if (store_dtype != LFFN_F32 && store_dtype != LFFN_BF16)
+    return fail(LFFN_ERR_USAGE, "tables upload: store dtype must be f32 or bf16");
+  if (host_dtype < LFFN_F32 || host_dtype > LFFN_F64)
+    return fail(LFFN_ERR_USAGE, "tables upload: unknown host dtype");
+  DeviceGuard g(c->device);
+  const size_t per_table = size_t(c->rows) * size_t(c->cfg.d_out);
+  const size_t count = per_table * size_t(c->h_loc);
+  const size_t first = per_table * size_t(c->kb);
+  const size_t esz = store_dtype == LFFN_F32 ? 4 : 2;
+  std::vector<unsigned char> staging(count * esz);
+  for (size_t i = 0; i < count; ++i) {
+    float f;
+    if (host_dtype == LFFN_F64) f = float(static_cast<const double*>(host_T)[first + i]);
+    else if (host_dtype == LFFN_F32) f = static_cast<const float*>(host_T)[first + i];
+    else f = bf16_to_f32(static_cast<const uint16_t*>(host_T)[first + i]);
+    if (store_dtype == LFFN_F32) {
+      std::memcpy(&staging[i * 4], &f, 4);
+    } else {
+      const uint16_t b = host_dtype == LFFN_BF16
+                             ? static_cast<const uint16_t*>(host_T)[first + i]
+                             : host_dtype == LFFN_F64
+                                   ? f64_to_bf16_rne(static_cast<const double*>(host_T)[first + i])
+                                   : f32_to_bf16_rne(f);
+      std::memcpy(&staging[i * 2], &b, 2);
+    }
+  }
+  if (c->d_T_owned) {
+    cudaFree(c->d_T_owned);
+    c->d_T_owned = nullptr;
+  }
+  void* d = nullptr;
+  LFFN_CUDA(cudaMalloc(&d, std::max<size_t>(staging.size(), 16)));
+  LFFN_CUDA(cudaMemcpy(d, staging.data(), staging.size(), cudaMemcpyHostToDevice));
+  c->d_T_owned = d;
+  c->d_T = d;
+  c->t_dtype = store_dtype;
+  return LFFN_OK;
+}
+
+int lffn_convert(const void* src, int src_dtype, void* dst, int dst_dtype, int64_t n) {
+  if ((!src || !dst) && n > 0) return fail(LFFN_ERR_USAGE, "convert: null buffer");
+  for (int64_t i = 0; i < n; ++i) {
+    double d;
+    if (src_dtype == LFFN_F64) d = static_cast<const double*>(src)[i];
+    else if (src_dtype == LFFN_F32) d = static_cast<const float*>(src)[i];
+    else if (src_dtype == LFFN_BF16) d = bf16_to_f32(static_cast<const uint16_t*>(src)[i]);
+    else return fail(LFFN_ERR_USAGE, "convert: unknown dtype");
+    if (dst_dtype == LFFN_F64) static_cast<double*>(dst)[i] = d;
+    else if (dst_dtype == LFFN_F32) static_cast<float*>(dst)[i] = float(d);
+    else if (dst_dtype == LFFN_BF16)
+      static_cast<uint16_t*>(dst)[i] = src_dtype == LFFN_F64 ? f64_to_bf16_rne(d) : f32_to_bf16_rne(float(d));
+    else return fail(LFFN_ERR_USAGE, "convert: unknown dtype");
+  }
+  return LFFN_OK;
+}
+
+int lffn_tables_attach(lffn_ctx* c, const void* d_T, int dtype) {
+  if (!c || !d_T) return fail(LFFN_ERR_USAGE, "tables attach: null argument");
+  if (dtype != LFFN_F32 && dtype != LFFN_BF16)
+    return fail(LFFN_ERR_USAGE, "tables attach: dtype must be f32 or bf16");
+  if (reinterpret_cast<uintptr_t>(d_T) % 16 != 0)
+    return fail(LFFN_ERR_USAGE, "tables attach: device buffer must be 16-byte aligned");
+  c->d_T = d_T;
+  c->t_dtype = dtype;
+  return LFFN_OK;
+}
+
+int lffn_hash(lffn_ctx* c, const float* d_x, int64_t n, uint32_t* d_codes, float* d_coeff,
+              double* d_z, void* stream) {
+  if (!c) return fail(LFFN_ERR_USAGE, "null context");
+  if (int rc = check_n(c, n)) return rc;
+  if (n > 0 && (!d_x || !d_codes || !d_coeff)) return fail(LFFN_ERR_USAGE, "hash: null buffer");
+  DeviceGuard g(c->device);
+  return launch_hash(c, d_x, n, d_codes, d_coeff, d_z, static_cast<cudaStream_t>(stream));
+}
+
+int lffn_lookup_accumulate(lffn_ctx* c, const uint32_t* d_codes, const float* d_coeff, int64_t n,
+                           float* d_y, int accumulate, void* stream) {
+  if (!c) return fail(LFFN_ERR_USAGE, "null context");
+  if (n < 0) return fail(LFFN_ERR_USAGE, "lookup accumulate: negative row count");
+  if (n > 0 && (!d_codes || !d_coeff || !d_y))
+    return fail(LFFN_ERR_USAGE, "lookup accumulate: null buffer");
+  DeviceGuard g(c->device);
+  return launch_gather(c, d_codes, d_coeff, n, d_y, accumulate ? 1 : 0,
+                       static_cast<cudaStream_t>(stream));
+}
+
+int lffn_forward(lffn_ctx* c, const float* d_x, int64_t n, float* d_y, void* stream) {
+  if (!c) return fail(LFFN_ERR_USAGE, "null context");
+  if (int rc = check_n(c, n)) return rc;
+  if (n > 0 && (!d_x || !d_y)) return fail(LFFN_ERR_USAGE, "forward: null buffer");
+  if (!c->d_T) return fail(LFFN_ERR_USAGE, "lookup forward: tables not uploaded");
+  DeviceGuard g(c->device);
+  return forward_impl(c, d_x, n, d_y, static_cast<cudaStream_t>(stream));
+}
+
+int lffn_forward_host(lffn_ctx* c, const float* h_x, int64_t n, float* h_y) {
+  if (!c) return fail(LFFN_ERR_USAGE, "null context");
+  if (int rc = check_n(c, n)) return rc;
+  if (n > 0 && (!h_x || !h_y)) return fail(LFFN_ERR_USAGE, "forward: null buffer");
+  if (!c->d_T) return fail(LFFN_ERR_USAGE, "lookup forward: tables not uploaded");
+  DeviceGuard g(c->device);
+  if (!c->d_xbuf) {
+    // first host-path call: I/O staging sized for max_tokens (allocated once)
+    LFFN_CUDA(cudaMalloc(&c->d_xbuf, size_t(std::max<int64_t>(c->max_tokens, 1)) * c->cfg.d_in * sizeof(float)));
+    LFFN_CUDA(cudaMalloc(&c->d_ybuf, size_t(std::max<int64_t>(c->max_tokens, 1)) * c->cfg.d_out * sizeof(float)));
+  }
+  if (n == 0) return LFFN_OK;
+  // Chunked pipeline: H2D(chunk i+1) || compute(chunk i) || D2H(chunk i-1).
+  const int64_t d_in = c->cfg.d_in, d_out = c->cfg.d_out;
+  int nch = int(std::min<int64_t>(lffn_ctx::kChunks, std::max<int64_t>(1, n / 1024)));
+  const int64_t per = (n + nch - 1) / nch;
+  for (int i = 0; i < nch; ++i) {
+    const int64_t r0 = i * per, r1 = std::min(n, r0 + per);
+    if (r0 >= r1) break;
+    LFFN_CUDA(cudaMemcpyAsync(c->d_xbuf + r0 * d_in, h_x + r0 * d_in,
+                              size_t(r1 - r0) * d_in * sizeof(float), cudaMemcpyHostToDevice, c->s_h2d));
+    LFFN_CUDA(cudaEventRecord(c->ev_h2d[i], c->s_h2d));
+    LFFN_CUDA(cudaStreamWaitEvent(c->s_comp, c->ev_h2d[i], 0));
+    if (int rc = launch_hash(c, c->d_xbuf + r0 * d_in, r1 - r0, c->d_codes + r0 * c->h_loc,
+                             c->d_coeff + r0 * c->h_loc, nullptr, c->s_comp))
+      return rc;
+    if (int rc = launch_gather(c, c->d_codes + r0 * c->h_loc, c->d_coeff + r0 * c->h_loc, r1 - r0,
+                               c->d_ybuf + r0 * d_out, 0, c->s_comp))
+      return rc;
+    LFFN_CUDA(cudaEventRecord(c->ev_comp[i], c->s_comp));
+    LFFN_CUDA(cudaStreamWaitEvent(c->s_d2h, c->ev_comp[i], 0));
+    LFFN_CUDA(cudaMemcpyAsync(h_y + r0 * d_out, c->d_ybuf + r0 * d_out,
+                              size_t(r1 - r0) * d_out * sizeof(float), cudaMemcpyDeviceToHost, c->s_d2h));
+  }
+  return read_flag(c, c->s_d2h);
+}
+
+int lffn_sync(lffn_ctx* c, void* stream) {
+  if (!c) return fail(LFFN_ERR_USAGE, "null context");
+  DeviceGuard g(c->device);
+  return read_flag(c, static_cast<cudaStream_t>(stream));
+}
+
+int lffn_ctx_set_timing(lffn_ctx* c, int enable) {
+  if (!c) return fail(LFFN_ERR_USAGE, "null context");
+  c->timing = enable != 0;
+  c->timed = false;
+  return LFFN_OK;
+}
+
+int lffn_ctx_stage_ms(lffn_ctx* c, float* hash_ms, float* gather_ms) {
+  if (!c) return fail(LFFN_ERR_USAGE, "null context");
+  if (!c->timed) {
+    if (hash_ms) *hash_ms = 0.f;
+    if (gather_ms) *gather_ms = 0.f;
+    return LFFN_OK;
+  }
+  DeviceGuard g(c->device);
+  LFFN_CUDA(cudaEventSynchronize(c->ev_t2));
+  float a = 0.f, b = 0.f;
+  LFFN_CUDA(cudaEventElapsedTime(&a, c->ev_t0, c->ev_t1));
+  LFFN_CUDA(cudaEventElapsedTime(&b, c->ev_t1, c->ev_t2));
+  if (hash_ms) *hash_ms = a;
+  if (gather_ms) *gather_ms = b;
+  return LFFN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,392 @@
+"""Host-side mirror of the reference's lookup API over the B200 C-ABI.
+
+Names, argument meaning and error behaviour follow the reference library
+(/root/reference/proj/include/lookupffn/{lookup,projection,common}.hpp) so that
+the reference's forward-path tests read the same against this package:
+
+=====================================  =========================================
+reference                               here
+=====================================  =========================================
+``LookupConfig`` (lookup.hpp:25-39)     ``LookupConfig``
+``LookupVariant`` (lookup.hpp:20)       ``LookupVariant``
+``ProjKind`` / ``ProjectionSpec``        ``ProjKind`` / ``ProjectionSpec``
+  (projection.hpp:13-37)
+``Projection::init / from_blob``        ``Projection.init / from_blob``
+  (projection.hpp:55-95)
+``HashTables::init / zeros_like /``     ``HashTables`` (same methods)
+  ``row / checksum`` (lookup.hpp:43-66)
+``lookup_forward`` (lookup.hpp:124)     ``lookup_forward`` (device; nc == 1)
+``SizeError / UsageError /``            ``SizeError / UsageError / NumericError``
+  ``NumericError`` (common.hpp:17-29)
+=====================================  =========================================
+
+Everything numeric runs in liblffn_gpu.so on the GPU; parameter generation
+uses the reference's own engine and libstdc++ distributions (host C++ inside
+the same library), so seeds give bit-identical parameters.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _capi
+from ._capi import LFFN_BF16, LFFN_F32, LFFN_F64, NumericError, SizeError, UsageError, check
+
+__all__ = [
+    "LookupVariant", "ProjKind", "LookupConfig", "ProjectionSpec", "Projection", "HashTables",
+    "LookupFFN", "lookup_forward", "fill_gaussian", "fill_signs", "gaussian_matrix",
+    "to_bf16_values", "SizeError", "UsageError", "NumericError",
+]
+
+
+class LookupVariant(enum.IntEnum):
+    softmax = 0
+    scaled = 1
+    sigmoid_tau1 = 2
+    gelu_tau1 = 3
+
+
+class ProjKind(enum.IntEnum):
+    dense = 0
+    bh = 1
+    acdc = 2
+    signflip = 3
+
+
+def _next_pow2(n: int) -> int:
+    p = 1
+    while p < n:
+        p <<= 1
+    return p
+
+
+@dataclass
+class LookupConfig:
+    d_in: int = 0
+    d_out: int = 0
+    tables: int = 1
+    code_bits: int = 1
+    variant: LookupVariant = LookupVariant.softmax
+    neighbor_count: int = 1
+
+    def code_width(self) -> int:
+        return self.tables * self.code_bits
+
+    def table_rows(self) -> int:
+        return 1 << self.code_bits
+
+    def scaled_numerator(self) -> bool:
+        return self.variant in (LookupVariant.scaled, LookupVariant.gelu_tau1)
+
+    def _c(self) -> _capi.lffn_cfg:
+        return _capi.lffn_cfg(self.d_in, self.d_out, self.tables, self.code_bits, int(self.variant),
+                              self.neighbor_count)
+
+    def validate(self) -> None:
+        check(_capi.lib().lffn_cfg_validate(C.byref(self._c())))
+
+
+@dataclass
+class ProjectionSpec:
+    d_in: int = 0
+    d_out: int = 0
+    kind: ProjKind = ProjKind.dense
+    stages: int = 4
+    block: int = 0
+    depth: int = 1
+
+    def transform_width(self) -> int:
+        return _next_pow2(max(self.d_in, self.d_out))
+
+    def _c(self, blob: Optional[np.ndarray] = None) -> _capi.lffn_proj:
+        p = _capi.lffn_proj(int(self.kind), 0, self.d_in, self.d_out, self.stages, self.block,
+                            self.depth, None, 0)
+        if blob is not None:
+            p.blob = blob.ctypes.data_as(C.POINTER(C.c_double))
+            p.blob_len = blob.size
+        return p
+
+    def validate(self) -> None:
+        check(_capi.lib().lffn_proj_validate(C.byref(self._c())))
+
+    def blob_size(self) -> int:
+        n = _capi.lib().lffn_proj_blob_size(C.byref(self._c()))
+        if n < 0:
+            check(_capi.LFFN_ERR_USAGE)
+        return int(n)
+
+    @staticmethod
+    def dense(d_in: int, d_out: int) -> "ProjectionSpec":
+        return ProjectionSpec(d_in, d_out, ProjKind.dense)
+
+    @staticmethod
+    def bh(d_in: int, d_out: int, m: int, b: int) -> "ProjectionSpec":
+        return ProjectionSpec(d_in, d_out, ProjKind.bh, stages=m, block=b)
+
+    @staticmethod
+    def acdc(d_in: int, d_out: int, k: int) -> "ProjectionSpec":
+        return ProjectionSpec(d_in, d_out, ProjKind.acdc, depth=k)
+
+    @staticmethod
+    def signflip(d_in: int, d_out: int) -> "ProjectionSpec":
+        return ProjectionSpec(d_in, d_out, ProjKind.signflip)
+
+
+@dataclass
+class Projection:
+    """A projection spec plus its float64 parameter blob (projection.hpp:47-54)."""
+
+    spec: ProjectionSpec
+    blob: np.ndarray = field(repr=False)
+
+    @staticmethod
+    def init(spec: ProjectionSpec, seed: int) -> "Projection":
+        spec.validate()
+        blob = np.empty(spec.blob_size(), np.float64)
+        check(_capi.lib().lffn_proj_init(C.byref(spec._c()), seed, blob.ctypes.data))
+        return Projection(spec, blob)
+
+    @staticmethod
+    def from_blob(spec: ProjectionSpec, blob) -> "Projection":
+        blob = np.ascontiguousarray(blob, np.float64).reshape(-1)
+        check(_capi.lib().lffn_proj_validate(C.byref(spec._c(blob))))
+        return Projection(spec, blob)
+
+    def params(self) -> np.ndarray:
+        return self.blob[:0] if self.spec.kind == ProjKind.signflip else self.blob
+
+    def _c(self) -> _capi.lffn_proj:
+        return self.spec._c(self.blob)
+
+
+@dataclass
+class HashTables:
+    """T, shape h x 2^tau x d_out, float64 host copy (lookup.hpp:43-66)."""
+
+    tables: int
+    code_bits: int
+    d_out: int
+    data: np.ndarray = field(repr=False)
+
+    def rows_per_table(self) -> int:
+        return 1 << self.code_bits
+
+    def row(self, k: int, code: int) -> np.ndarray:
+        r = self.rows_per_table()
+        o = (k * r + code) * self.d_out
+        return self.data[o:o + self.d_out]
+
+    @staticmethod
+    def init(cfg: LookupConfig, seed: int) -> "HashTables":
+        cfg.validate()
+        data = np.empty(cfg.tables * cfg.table_rows() * cfg.d_out, np.float64)
+        check(_capi.lib().lffn_tables_init(C.byref(cfg._c()), seed, data.ctypes.data))
+        return HashTables(cfg.tables, cfg.code_bits, cfg.d_out, data)
+
+    @staticmethod
+    def zeros_like(cfg: LookupConfig) -> "HashTables":
+        return HashTables(cfg.tables, cfg.code_bits, cfg.d_out,
+                          np.zeros(cfg.tables * cfg.table_rows() * cfg.d_out, np.float64))
+
+    def checksum(self) -> int:
+        """FNV-1a over the raw float64 bytes (lookup.cpp:60-68)."""
+        h = 1469598103934665603
+        for b in self.data.tobytes():
+            h ^= b
+            h = (h * 1099511628211) & 0xFFFFFFFFFFFFFFFF
+        return h
+
+
+def fill_gaussian(seed: int, n: int, stddev: float = 1.0) -> np.ndarray:
+    """make_rng(seed) + fill_gaussian (common.hpp:44-49), bit-identical."""
+    out = np.empty(n, np.float64)
+    check(_capi.lib().lffn_fill_gaussian(seed, out.ctypes.data, n, stddev))
+    return out
+
+
+def fill_signs(seed: int, n: int) -> np.ndarray:
+    out = np.empty(n, np.float64)
+    check(_capi.lib().lffn_fill_signs(seed, out.ctypes.data, n))
+    return out
+
+
+def gaussian_matrix(rows: int, cols: int, seed: int, stddev: float = 1.0) -> np.ndarray:
+    """DenseMatrix::gaussian(rows, cols, make_rng(seed), stddev) (matrix.hpp:37-42)."""
+    return fill_gaussian(seed, rows * cols, stddev).reshape(rows, cols)
+
+
+def to_bf16_values(a: np.ndarray) -> np.ndarray:
+    """The float64 values a bf16 table upload stores (single RNE rounding)."""
+    a = np.ascontiguousarray(a, np.float64).reshape(-1)
+    bits = np.empty(a.size, np.uint16)
+    check(_capi.lib().lffn_convert(a.ctypes.data, LFFN_F64, bits.ctypes.data, LFFN_BF16, a.size))
+    return (bits.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+
+
+_DTYPES = {"f32": LFFN_F32, "float32": LFFN_F32, "bf16": LFFN_BF16, "bfloat16": LFFN_BF16}
+
+
+class LookupFFN:
+    """A device-resident LookupFFN layer: one lffn_ctx on one GPU.
+
+    ``table_range=(kb, ke)`` makes a table shard (multi-GPU table sharding):
+    the layer then produces the partial sum over tables [kb, ke).
+    """
+
+    def __init__(self, cfg: LookupConfig, proj: Projection, tables, *, device: int = 0,
+                 max_tokens: int = 65536, table_dtype: str = "f32",
+                 table_range: Optional[tuple] = None):
+        cfg.validate()
+        self.cfg, self.proj, self.device = cfg, proj, device
+        self.max_tokens = max_tokens
+        self.table_dtype = _DTYPES[table_dtype]
+        L = _capi.lib()
+        ctx = C.c_void_p()
+        kb, ke = table_range if table_range is not None else (0, cfg.tables)
+        check(L.lffn_ctx_create_shard(C.byref(ctx), device, max_tokens, C.byref(cfg._c()),
+                                      C.byref(proj._c()), kb, ke))
+        self._ctx = ctx
+        self.table_range = (kb, ke)
+        if tables is not None:
+            self.upload_tables(tables)
+
+    # -- tables ----------------------------------------------------------
+    def upload_tables(self, tables) -> None:
+        """Upload the FULL h x 2^tau x d_out stack (HashTables or ndarray)."""
+        data = tables.data if isinstance(tables, HashTables) else tables
+        if hasattr(data, "detach"):
+            data = data.detach().cpu().numpy()
+        data = np.ascontiguousarray(data)
+        expect = self.cfg.tables * self.cfg.table_rows() * self.cfg.d_out
+        if data.size != expect:
+            raise SizeError("lookup forward: table stack shape mismatch")
+        if data.dtype == np.float64:
+            host = LFFN_F64
+        elif data.dtype == np.float32:
+            host = LFFN_F32
+        elif data.dtype == np.uint16:
+            host = LFFN_BF16
+        else:
+            raise UsageError(f"unsupported table dtype {data.dtype}")
+        check(_capi.lib().lffn_tables_upload(self._ctx, data.ctypes.data, host, self.table_dtype))
+
+    def attach_tables(self, dev_tensor) -> None:
+        """Use a caller-owned device tensor holding this shard's slice (no copy)."""
+        import torch
+
+        dt = LFFN_F32 if dev_tensor.dtype == torch.float32 else LFFN_BF16
+        self._tables_ref = dev_tensor
+        self.table_dtype = dt
+        check(_capi.lib().lffn_tables_attach(self._ctx, dev_tensor.data_ptr(), dt))
+
+    # -- device-pointer API (torch tensors on this GPU) -----------------
+    @staticmethod
+    def _stream(stream) -> int:
+        if stream is None:
+            import torch
+
+            return torch.cuda.current_stream().cuda_stream
+        return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+    def hash(self, x, codes=None, coeff=None, z=None, stream=None):
+        """lffn_hash on device tensors; returns (codes, coeff[, z])."""
+        import torch
+
+        n = x.shape[0]
+        hl = self.table_range[1] - self.table_range[0]
+        dev = x.device
+        if codes is None:
+            codes = torch.empty((n, hl), dtype=torch.int32, device=dev)
+        if coeff is None:
+            coeff = torch.empty((n, hl), dtype=torch.float32, device=dev)
+        zp = z.data_ptr() if z is not None else None
+        check(_capi.lib().lffn_hash(self._ctx, x.data_ptr(), n, codes.data_ptr(), coeff.data_ptr(),
+                                    zp, self._stream(stream)))
+        return (codes, coeff) if z is None else (codes, coeff, z)
+
+    def lookup_accumulate(self, codes, coeff, y, accumulate: bool = False, stream=None):
+        n = codes.shape[0]
+        check(_capi.lib().lffn_lookup_accumulate(self._ctx, codes.data_ptr(), coeff.data_ptr(), n,
+                                                 y.data_ptr(), int(accumulate),
+                                                 self._stream(stream)))
+        return y
+
+    def forward_device(self, x, y=None, stream=None):
+        import torch
+
+        if y is None:
+            y = torch.empty((x.shape[0], self.cfg.d_out), dtype=torch.float32, device=x.device)
+        check(_capi.lib().lffn_forward(self._ctx, x.data_ptr(), x.shape[0], y.data_ptr(),
+                                       self._stream(stream)))
+        return y
+
+    def sync(self, stream=None) -> None:
+        check(_capi.lib().lffn_sync(self._ctx, self._stream(stream)))
+
+    # -- host API (the reference's call shape) ---------------------------
+    def forward(self, x: np.ndarray, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """y = lookup_forward(x) with host float32 buffers (H2D/D2H inside)."""
+        x = np.ascontiguousarray(x, np.float32)
+        if x.ndim != 2 or x.shape[1] != self.cfg.d_in:
+            raise SizeError("lookup forward: input width mismatch")
+        if out is None:
+            out = np.empty((x.shape[0], self.cfg.d_out), np.float32)
+        check(_capi.lib().lffn_forward_host(self._ctx, x.ctypes.data, x.shape[0], out.ctypes.data))
+        return out
+
+    def forward_host_ptr(self, x_ptr: int, n: int, y_ptr: int) -> None:
+        check(_capi.lib().lffn_forward_host(self._ctx, x_ptr, n, y_ptr))
+
+    def launch_count(self) -> int:
+        return int(_capi.lib().lffn_ctx_launch_count(self._ctx))
+
+    def set_timing(self, on: bool) -> None:
+        check(_capi.lib().lffn_ctx_set_timing(self._ctx, int(on)))
+
+    def stage_ms(self):
+        a, b = C.c_float(), C.c_float()
+        check(_capi.lib().lffn_ctx_stage_ms(self._ctx, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def close(self) -> None:
+        if getattr(self, "_ctx", None):
+            _capi.lib().lffn_ctx_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def lookup_forward(x, proj: Projection, tables: HashTables, cfg: LookupConfig,
+                   cache=None, *, device: int = 0, table_dtype: str = "f32") -> np.ndarray:
+    """Drop-in for lffn::lookup_forward (lookup.hpp:124-125), top-1 only.
+
+    Returns y as float64 (the reference returns a DenseMatrix of doubles); the
+    device computes it with fp32 tables/accumulators.  ``cache`` is the
+    reference's training-only LookupCache and is rejected, as is nc > 1:
+    there is no CPU fallback.
+    """
+    if cache is not None:
+        raise UsageError("lookup forward: LookupCache (training) is not supported on the device path")
+    cfg.validate()
+    x = np.asarray(x)
+    if x.ndim != 2 or x.shape[1] != cfg.d_in:
+        raise SizeError("lookup forward: input width mismatch")
+    if proj.spec.d_in != cfg.d_in or proj.spec.d_out != cfg.code_width():
+        raise SizeError("lookup forward: projection must map d_in to h*tau")
+    if (tables.tables, tables.code_bits, tables.d_out) != (cfg.tables, cfg.code_bits, cfg.d_out):
+        raise SizeError("lookup forward: table stack shape mismatch")
+    layer = LookupFFN(cfg, proj, tables, device=device, max_tokens=max(1, x.shape[0]),
+                      table_dtype=table_dtype)
+    try:
+        y = layer.forward(np.ascontiguousarray(x, np.float32))
+    finally:
+        layer.close()
+    return y.astype(np.float64)
