@@ -175,6 +175,11 @@ int64_t lffn_ctx_launch_count(const lffn_ctx* ctx);
 int lffn_ctx_set_timing(lffn_ctx* ctx, int enable);
 int lffn_ctx_stage_ms(lffn_ctx* ctx, float* hash_ms, float* gather_ms);
 
+/* Bandwidth probe for the roofline denominators (no reference counterpart):
+ * which = 0 L2 read GB/s (32 MiB re-read from every SM), 1 HBM read GB/s
+ * (4 GiB stream); best of reps CUDA-event-timed launches. */
+int lffn_probe_bandwidth(int device, int which, int reps, double* gbs);
+
 /* Thread-local message for the last non-zero status. */
 const char* lffn_last_error(void);
 

@@ -59,6 +59,7 @@ SIGNATURES = {
     "lffn_ctx_launch_count": (_I64, [_VP]),
     "lffn_ctx_set_timing": (C.c_int, [_VP, C.c_int]),
     "lffn_ctx_stage_ms": (C.c_int, [_VP, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
+    "lffn_probe_bandwidth": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]),
     "lffn_last_error": (C.c_char_p, []),
     "lffn_version": (C.c_char_p, []),
 }
