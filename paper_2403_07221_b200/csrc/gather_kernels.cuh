@@ -129,4 +129,117 @@ __global__ void __launch_bounds__(256) gather_direct_kernel(GatherParams p) {
   if (bad) atomicOr(p.flag, bad);
 }
 
+// Row-per-warp gather: one warp owns one token and up to MAXC chunks of
+// 32*VEC columns of its output row (several warps per token for wide rows).
+// Per table every lane issues its MAXC 128-bit row loads back to back; two
+// tables are in flight at once, and the (code, coeff) records of the next
+// four tables are prefetched while the current four are consumed, so no
+// row load waits on a dependent record load.  Small per-warp register
+// footprint -> high occupancy -> many L2 requests in flight per SM.
+template <typename TT, int VEC, int MAXC, bool REC4>
+__global__ void __launch_bounds__(256) gather_row_kernel(GatherParams p, int warps_per_token) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t token = gwarp / warps_per_token;
+  if (token >= p.n) return;
+  const int part = (int)(gwarp - token * warps_per_token);
+  constexpr int CHUNK = 32 * VEC;
+  const int nchunks = (p.d_out + CHUNK - 1) / CHUNK;
+  const int c0 = part * MAXC;
+  const int nck = min(MAXC, nchunks - c0);
+  const int colbase = c0 * CHUNK + lane * VEC;
+  const TT* T = reinterpret_cast<const TT*>(p.T);
+  const int64_t tstride = (int64_t)p.rows * p.d_out;
+  const uint32_t* cr = p.codes + token * p.h_loc;
+  const float* wr = p.coeff + token * p.h_loc;
+
+  float acc[MAXC][VEC];
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c)
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) acc[c][v] = 0.f;
+
+  auto row_loads = [&](int k, uint32_t code, float (&vals)[MAXC][VEC]) {
+    const TT* rp = T + k * tstride + (int64_t)code * p.d_out + colbase;
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+      if (c < nck && colbase + c * CHUNK < p.d_out) RowLoad<TT, VEC>::load(rp + c * CHUNK, vals[c]);
+      else {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) vals[c][v] = 0.f;
+      }
+    }
+  };
+  auto fma_row = [&](float w, const float (&vals)[MAXC][VEC]) {
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) acc[c][v] = fmaf(w, vals[c][v], acc[c][v]);
+  };
+
+  if constexpr (REC4) {
+    // records of 4 tables per 128-bit broadcast load
+    uint4 cc = __ldg(reinterpret_cast<const uint4*>(cr));
+    float4 ww = __ldg(reinterpret_cast<const float4*>(wr));
+    for (int kg = 0; kg < p.h_loc; kg += 4) {
+      uint4 cn = cc;
+      float4 wn = ww;
+      if (kg + 4 < p.h_loc) {
+        cn = __ldg(reinterpret_cast<const uint4*>(cr + kg + 4));
+        wn = __ldg(reinterpret_cast<const float4*>(wr + kg + 4));
+      }
+      float va[MAXC][VEC], vb[MAXC][VEC];
+      row_loads(kg + 0, cc.x, va);
+      row_loads(kg + 1, cc.y, vb);
+      fma_row(ww.x, va);
+      fma_row(ww.y, vb);
+      row_loads(kg + 2, cc.z, va);
+      row_loads(kg + 3, cc.w, vb);
+      fma_row(ww.z, va);
+      fma_row(ww.w, vb);
+      cc = cn;
+      ww = wn;
+    }
+  } else {
+    uint32_t cc = __ldg(cr);
+    float ww = __ldg(wr);
+    for (int k = 0; k < p.h_loc; ++k) {
+      uint32_t cn = cc;
+      float wn = ww;
+      if (k + 1 < p.h_loc) {
+        cn = __ldg(cr + k + 1);
+        wn = __ldg(wr + k + 1);
+      }
+      float va[MAXC][VEC];
+      row_loads(k, cc, va);
+      fma_row(ww, va);
+      cc = cn;
+      ww = wn;
+    }
+  }
+
+  int bad = 0;
+  float* yr = p.y + token * p.d_out;
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c) {
+    const int col = colbase + c * CHUNK;
+    if (c < nck && col < p.d_out) {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        float o = acc[c][v];
+        if (p.accumulate) o += yr[col + v];
+        if (!isfinite(o)) bad = 4;
+        acc[c][v] = o;
+      }
+      if constexpr (VEC == 4) {
+        *reinterpret_cast<float4*>(yr + col) = make_float4(acc[c][0], acc[c][1], acc[c][2], acc[c][3]);
+      } else {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) yr[col + v] = acc[c][v];
+      }
+    }
+  }
+  if (bad) atomicOr(p.flag, bad);
+}
+
 }  // namespace lffn_gpu

@@ -15,6 +15,14 @@
 // bit-identical to the reference's double Projection::forward.  Codes are
 // therefore bit-exact; the coefficient differs from the reference only by
 // the last-bit behaviour of the device exp().
+//
+// Data movement: each token's D-vector lives in shared memory (padded one
+// double per 64).  A thread owns E = min(64, D) elements; a "phase" loads
+// them, applies up to log2(E) consecutive butterfly stages in registers and
+// stores them back, so a D = 2048 transform is two shared-memory round trips
+// (bits 0-5, then bits 6-10) and D = 4096 is two as well.  Both access
+// patterns (64 consecutive elements per thread; consecutive elements across
+// threads) are bank-conflict free with the 65-double stride.
 #pragma once
 
 #include <cstdint>
@@ -43,21 +51,24 @@ struct HashParams {
   int threads_per_token;
 };
 
-// Padded shared-memory position: one spare double per 16 keeps both the
-// contiguous (phase 0) and the strided (later phases) access patterns free
-// of bank conflicts.
-__device__ __forceinline__ int spos(int a) { return a + (a >> 4); }
+constexpr int kMaxLogE = 6;
 
-__device__ __forceinline__ double flip_sign(double v, uint32_t bit) {
-  // multiply by -1.0 when bit is set: exact, equal to the reference's
-  // buf[j] *= sv[j] with sv = -1.0
-  unsigned long long u = __double_as_longlong(v);
-  u ^= (unsigned long long)bit << 63;
-  return __longlong_as_double(u);
+// Padded shared-memory position: two spare doubles per 64 elements.  A
+// thread's 64 consecutive elements (phase 0) then start 66 doubles apart
+// (16-byte aligned, conflict-free 128-bit accesses per quarter warp), and
+// element pairs (a, a+1) stay adjacent for the later phases.
+__device__ __forceinline__ int spos(int a) { return a + 2 * (a >> 6); }
+__host__ __device__ constexpr int padded_len(int D) { return D + 2 * (D >> 6); }
+
+// Multiply by -1.0 when bit `sh` of m is set -- exact, and equal to the
+// reference's buf[j] *= sv[j] with sv = -1.0 (including 0.0 -> -0.0): the
+// sign bit of the high word is XORed with the mask bit moved to bit 31.
+__device__ __forceinline__ double flip_sign(double v, uint32_t m, int sh) {
+  const int hi = __double2hiint(v) ^ (int)((m << (31 - sh)) & 0x80000000u);
+  return __hiloint2double(hi, __double2loint(v));
 }
 
-// One phase: B consecutive transform bits [lo, lo+B) applied to this
-// thread's E = 2^LOGE elements held as E/2^B groups of 2^B.
+// B consecutive transform bits applied to E/2^B register groups of 2^B.
 template <int LOGE, int B>
 __device__ __forceinline__ void butterfly_groups(double (&v)[1 << LOGE]) {
   constexpr int E = 1 << LOGE;
@@ -80,59 +91,168 @@ __device__ __forceinline__ void butterfly_groups(double (&v)[1 << LOGE]) {
   }
 }
 
-// Element index of register slot r (group grp = r / G, member i = r % G) for
-// thread t of a token in the phase with bits [lo, lo+B).
-template <int B>
-__device__ __forceinline__ int phase_index(int t, int tpt, int grp, int i, int lo) {
-  const int g = t + grp * tpt;
-  const int glow = g & ((1 << lo) - 1);
-  const int ghigh = g >> lo;
-  return glow | (i << lo) | (ghigh << (lo + B));
+// Shared-memory traffic of one phase over transform bits [lo, lo+B): the
+// thread's E = 2^LOGE registers are J = E/2^B groups g = grp + J*t of 2^B
+// elements a = glow | i << lo | ghigh << (lo+B) (glow = g mod 2^lo).  Every
+// position is base[grp] + i * stride, and consecutive groups (grp, grp+1)
+// are adjacent doubles, so the traffic is 128-bit LDS/STS pairs.
+template <int LOGE, int B, bool STORE>
+__device__ __forceinline__ void phase_io(double* sm, double (&v)[1 << LOGE], int t, int lo) {
+  constexpr int E = 1 << LOGE;
+  constexpr int G = 1 << B;
+  constexpr int J = E / G;
+  if (lo == 0) {
+    // phase 0 (J == 1): elements t*E .. t*E + E-1, contiguous after padding
+    if constexpr (J == 1) {
+      double* q = sm + spos(t * E);
+      if constexpr (E >= 2) {
+#pragma unroll
+        for (int i = 0; i < E; i += 2) {
+          double2* d = reinterpret_cast<double2*>(q + i);
+          if constexpr (STORE) *d = make_double2(v[i], v[i + 1]);
+          else { const double2 w = *d; v[i] = w.x; v[i + 1] = w.y; }
+        }
+      } else {
+        if constexpr (STORE) q[0] = v[0];
+        else v[0] = q[0];
+      }
+    }
+    return;
+  }
+  if (lo >= 6) {
+    // the padding term is linear in i: position = base + i * stride
+    const int stride = (1 << lo) + (1 << (lo - 5));
+    if constexpr (J == 1) {
+      const int glow = t & ((1 << lo) - 1);
+      const int base = glow + 2 * (glow >> 6) + (t >> lo) * ((1 << (lo + B)) + (1 << (lo + B - 5)));
+#pragma unroll
+      for (int i = 0; i < G; ++i) {
+        if constexpr (STORE) sm[base + i * stride] = v[i];
+        else v[i] = sm[base + i * stride];
+      }
+    } else {
+#pragma unroll
+      for (int grp = 0; grp < J; grp += 2) {
+        const int g = grp + J * t;
+        const int glow = g & ((1 << lo) - 1);
+        const int base = glow + 2 * (glow >> 6) + (g >> lo) * ((1 << (lo + B)) + (1 << (lo + B - 5)));
+#pragma unroll
+        for (int i = 0; i < G; ++i) {
+          double2* d = reinterpret_cast<double2*>(sm + base + i * stride);
+          if constexpr (STORE) *d = make_double2(v[grp * G + i], v[(grp + 1) * G + i]);
+          else { const double2 w = *d; v[grp * G + i] = w.x; v[(grp + 1) * G + i] = w.y; }
+        }
+      }
+    }
+    return;
+  }
+  // 0 < lo < 6 (LOGE < 6 with several phases): generic positions
+#pragma unroll
+  for (int grp = 0; grp < J; ++grp) {
+    const int g = grp + J * t;
+    const int glow = g & ((1 << lo) - 1);
+    const int ghigh = g >> lo;
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+      const int pos = spos(glow | (i << lo) | (ghigh << (lo + B)));
+      if constexpr (STORE) sm[pos] = v[grp * G + i];
+      else v[grp * G + i] = sm[pos];
+    }
+  }
 }
 
-template <int LOGE, int B>
-__device__ __forceinline__ void phase_smem(double* sm, int t, int tpt, int lo, bool first_of_tr,
-                                           const HashParams& p, int tr) {
+enum : int { kPreNone = 0, kPreSign = 1, kPreDiag = 2 };
+
+// One phase over transform bits [lo, lo+B).  SRC_X: the token's inputs come
+// straight from x (very first phase); PRE: the elementwise factor applied
+// before a transform (signflip sign flip / acdc diagonal), phase 0 only.
+template <int LOGE, int B, bool SRC_X, int PRE>
+__device__ __forceinline__ void phase_smem(double* sm, int t, int tpt, int lo, const HashParams& p,
+                                           int tr, const float* xr, int& bad) {
   constexpr int E = 1 << LOGE;
   constexpr int G = 1 << B;
   double v[E];
+  if constexpr (SRC_X) {
+    // pad x to D (projection.cpp:212-213), fp32 -> fp64 exactly (lo == 0:
+    // this thread's elements are t*E .. t*E+E-1)
+    if (t * E + E <= p.d_in && (p.d_in & 3) == 0) {
 #pragma unroll
-  for (int r = 0; r < E; ++r) v[r] = sm[spos(phase_index<B>(t, tpt, r / G, r % G, lo))];
-  if (first_of_tr) {
-    // phase 0 of a transform: lo == 0, B == LOGE, elements t*E .. t*E+E-1
-    if (p.signmask) {
-      const int words = (p.D + 31) >> 5;
-      const int a0 = t * E;
-      const uint32_t m = __ldg(p.signmask + tr * words + (a0 >> 5)) >> (a0 & 31);
-#pragma unroll
-      for (int r = 0; r < E; ++r) v[r] = flip_sign(v[r], (m >> r) & 1u);
-    } else if (p.diag) {
-      const double* dg = p.diag + (size_t)tr * p.D + t * E;
-#pragma unroll
-      for (int r = 0; r < E; ++r) v[r] = __dmul_rn(v[r], __ldg(dg + r));
+      for (int r = 0; r < E; r += 4) {
+        const float4 f = __ldg(reinterpret_cast<const float4*>(xr + t * E + r));
+        if (!isfinite(f.x) || !isfinite(f.y) || !isfinite(f.z) || !isfinite(f.w)) bad |= 1;
+        v[r] = (double)f.x;
+        v[r + 1] = (double)f.y;
+        v[r + 2] = (double)f.z;
+        v[r + 3] = (double)f.w;
+      }
+    } else {
+#pragma unroll 8
+      for (int r = 0; r < E; ++r) {
+        const int a = t * E + r;
+        double xv = 0.0;
+        if (a < p.d_in) {
+          const float f = __ldg(xr + a);
+          if (!isfinite(f)) bad |= 1;
+          xv = (double)f;
+        }
+        v[r] = xv;
+      }
     }
+  } else {
+    phase_io<LOGE, B, false>(sm, v, t, lo);
+  }
+  if constexpr (PRE == kPreSign) {
+    const int words = (p.D + 31) >> 5;
+    const uint32_t* mw = p.signmask + tr * words;
+#pragma unroll
+    for (int r0 = 0; r0 < E; r0 += 32) {
+      const int a0 = t * E + r0;
+      const uint32_t m = __ldg(mw + (a0 >> 5)) >> (a0 & 31);
+#pragma unroll
+      for (int r = r0; r < r0 + 32 && r < E; ++r) v[r] = flip_sign(v[r], m, r - r0);
+    }
+  } else if constexpr (PRE == kPreDiag) {
+    const double* dg = p.diag + (size_t)tr * p.D + t * E;
+#pragma unroll
+    for (int r = 0; r < E; ++r) v[r] = __dmul_rn(v[r], __ldg(dg + r));
   }
   butterfly_groups<LOGE, B>(v);
-#pragma unroll
-  for (int r = 0; r < E; ++r) sm[spos(phase_index<B>(t, tpt, r / G, r % G, lo))] = v[r];
+  phase_io<LOGE, B, true>(sm, v, t, lo);
 }
 
+// Phase 0 of transform tr (bits [0, LOGE)) -- the pre-factor phase.
+template <int LOGE, int PRE>
+__device__ __forceinline__ void run_first_phase(double* sm, int t, int tpt, const HashParams& p,
+                                                int tr, const float* xr, int& bad) {
+  if (tr == 0) phase_smem<LOGE, LOGE, true, PRE>(sm, t, tpt, 0, p, tr, xr, bad);
+  else phase_smem<LOGE, LOGE, false, PRE>(sm, t, tpt, 0, p, tr, xr, bad);
+}
+
+// Later phases (bits [lo, lo+b), b <= LOGE).
 template <int LOGE>
-__device__ __forceinline__ void run_phase(double* sm, int t, int tpt, int lo, int b,
-                                          bool first_of_tr, const HashParams& p, int tr) {
-  if constexpr (LOGE >= 4) { if (b == 4) { phase_smem<LOGE, 4>(sm, t, tpt, lo, first_of_tr, p, tr); return; } }
-  if constexpr (LOGE >= 3) { if (b == 3) { phase_smem<LOGE, 3>(sm, t, tpt, lo, first_of_tr, p, tr); return; } }
-  if constexpr (LOGE >= 2) { if (b == 2) { phase_smem<LOGE, 2>(sm, t, tpt, lo, first_of_tr, p, tr); return; } }
-  if constexpr (LOGE >= 1) { if (b == 1) { phase_smem<LOGE, 1>(sm, t, tpt, lo, first_of_tr, p, tr); return; } }
-  if (b == 0 && first_of_tr) phase_smem<LOGE, 0>(sm, t, tpt, lo, first_of_tr, p, tr);
+__device__ __forceinline__ void run_later_phase(double* sm, int t, int tpt, int lo, int b,
+                                                const HashParams& p, int tr, int& bad) {
+  if constexpr (LOGE >= 6) { if (b == 6) { phase_smem<LOGE, 6, false, kPreNone>(sm, t, tpt, lo, p, tr, nullptr, bad); return; } }
+  if constexpr (LOGE >= 5) { if (b == 5) { phase_smem<LOGE, 5, false, kPreNone>(sm, t, tpt, lo, p, tr, nullptr, bad); return; } }
+  if constexpr (LOGE >= 4) { if (b == 4) { phase_smem<LOGE, 4, false, kPreNone>(sm, t, tpt, lo, p, tr, nullptr, bad); return; } }
+  if constexpr (LOGE >= 3) { if (b == 3) { phase_smem<LOGE, 3, false, kPreNone>(sm, t, tpt, lo, p, tr, nullptr, bad); return; } }
+  if constexpr (LOGE >= 2) { if (b == 2) { phase_smem<LOGE, 2, false, kPreNone>(sm, t, tpt, lo, p, tr, nullptr, bad); return; } }
+  if constexpr (LOGE >= 1) { if (b == 1) { phase_smem<LOGE, 1, false, kPreNone>(sm, t, tpt, lo, p, tr, nullptr, bad); return; } }
 }
 
-// Codes + coefficient for one (token, table) from its tau soft-code
-// coordinates (lookup.cpp:81-100, 185-189, 241-253).
+// 1 + exp(-2a), kept out of line: it is needed only for |z| < 18.5 (rare
+// for the unnormalised transforms), and inlining it per coordinate bloats
+// the kernel past the instruction cache.
+__device__ __noinline__ double one_plus_exp_m2(double a) { return __dadd_rn(1.0, exp(-2.0 * a)); }
+
+// Code + coefficient of one (token, table) from its tau soft-code
+// coordinates (lookup.cpp:81-100, 185-189, 241-253), coordinates in the
+// reference's order j = 0 .. tau-1.
 __device__ __forceinline__ void code_and_coeff(const double* sm, int base, int tau, int scaled,
                                                uint32_t* code_out, float* coeff_out) {
   uint32_t code = 0;
   double w = 1.0, sum_abs = 0.0;
+#pragma unroll 1
   for (int j = 0; j < tau; ++j) {
     const double zj = sm[spos(base + j)];
     if (zj >= 0.0) code |= (1u << j);
@@ -140,19 +260,17 @@ __device__ __forceinline__ void code_and_coeff(const double* sm, int base, int t
     sum_abs = __dadd_rn(sum_abs, a);
     // 1 + exp(-2a) == 1.0 exactly once exp(-2a) <= 2^-53 (a >= 18.37):
     // dividing by 1.0 is then a no-op, so skipping the exp is exact.
-    if (a < 18.5) w = __ddiv_rn(w, __dadd_rn(1.0, exp(-2.0 * a)));
+    if (a < 18.5) w = __ddiv_rn(w, one_plus_exp_m2(a));
   }
   *code_out = code;
   *coeff_out = (float)(scaled ? __dmul_rn(w, sum_abs) : w);
 }
 
 // K1 for structured projections (signflip, acdc) and the epilogue of the
-// dense projection (z_in given): one CTA holds tokens_per_block token
-// vectors of D doubles in shared memory; every phase loads 2^LOGE elements
-// per thread, applies up to LOGE butterfly stages in registers and stores
-// them back, so log2(D)/LOGE shared-memory round trips per transform.
-template <int LOGE>
-__global__ void __launch_bounds__(1024) hash_structured_kernel(HashParams p) {
+// dense projection (z_in given).
+// KIND: kPreSign (signflip), kPreDiag (acdc), kPreNone (dense epilogue on z_in).
+template <int LOGE, int KIND>
+__global__ void __launch_bounds__(256) hash_structured_kernel(HashParams p) {
   extern __shared__ double smem[];
   constexpr int E = 1 << LOGE;
   const int tpt = p.threads_per_token;
@@ -161,56 +279,55 @@ __global__ void __launch_bounds__(1024) hash_structured_kernel(HashParams p) {
   const int64_t token = (int64_t)blockIdx.x * p.tokens_per_block + slot;
   const bool active = slot < p.tokens_per_block && token < p.n;
   const int D = p.D;
-  double* sm = smem + (size_t)slot * (D + (D >> 4));
+  double* sm = smem + (size_t)slot * padded_len(D);
   int bad = 0;
 
-  if (p.z_in) {
+  // Only the threads of one token share its vector, so phases synchronise
+  // per token: the warp when a token fits in one, else a named barrier.
+  auto token_sync = [&]() {
+    if (tpt <= 32) __syncwarp();
+    else asm volatile("bar.sync %0, %1;" ::"r"(slot + 1), "r"(tpt) : "memory");
+  };
+
+  if constexpr (KIND == kPreNone) {
     // dense: z already computed; stage the token's z row into smem
     if (active)
       for (int a = t; a < p.code_width; a += tpt) sm[spos(a)] = p.z_in[token * p.code_width + a];
-  } else if (active) {
-    // pad x to D (projection.cpp:212-213), fp32 -> fp64 exactly
+    token_sync();
+  } else {
     const float* xr = p.x + token * (int64_t)p.d_in;
-#pragma unroll
-    for (int r = 0; r < E; ++r) {
-      const int a = t * E + r;
-      double v = 0.0;
-      if (a < p.d_in) {
-        const float xv = __ldg(xr + a);
-        if (!isfinite(xv)) bad |= 1;
-        v = (double)xv;
-      }
-      sm[spos(a)] = v;
-    }
-  }
-  __syncthreads();
-
-  if (!p.z_in) {
     int nph = 1;
     if constexpr (LOGE > 0) nph = (p.logD + LOGE - 1) / LOGE;
     for (int tr = 0; tr < p.n_transforms; ++tr) {
-      for (int ph = 0; ph < nph; ++ph) {
+      if (active) run_first_phase<LOGE, KIND>(sm, t, tpt, p, tr, xr, bad);
+      token_sync();
+      for (int ph = 1; ph < nph; ++ph) {
         const int lo = ph * LOGE;
-        const int b = min(LOGE, p.logD - lo);
-        if (active) run_phase<LOGE>(sm, t, tpt, lo, b, ph == 0, p, tr);
-        __syncthreads();
+        if (active) run_later_phase<LOGE>(sm, t, tpt, lo, min(LOGE, p.logD - lo), p, tr, bad);
+        token_sync();
       }
     }
   }
 
   if (active) {
     // finiteness of the whole projection output (projection.cpp:264,
-    // lookup.cpp:204) and the optional z copy-out
+    // lookup.cpp:204) and the optional z copy-out, coalesced
     for (int a = t; a < p.code_width; a += tpt) {
       const double zv = sm[spos(a)];
       if (!isfinite(zv)) bad |= 2;
       if (p.z_out) p.z_out[token * p.code_width + a] = zv;
     }
+    // each table is finished by the thread whose element range holds its
+    // first coordinate; with the 65-double stride the sequential reads of
+    // neighbouring threads stay (nearly) bank-conflict free
+    const int tau = p.tau;
     const int hl = p.ke - p.kb;
-    for (int k = p.kb + t; k < p.ke; k += tpt) {
+    const int a_lo = t * E;
+    const int a_hi = min(a_lo + E, p.code_width);
+    for (int k = max((a_lo + tau - 1) / tau, p.kb); k < p.ke && k * tau < a_hi; ++k) {
       uint32_t code;
       float cf;
-      code_and_coeff(sm, k * p.tau, p.tau, p.scaled, &code, &cf);
+      code_and_coeff(sm, k * tau, tau, p.scaled, &code, &cf);
       p.codes[token * hl + (k - p.kb)] = code;
       p.coeff[token * hl + (k - p.kb)] = cf;
     }

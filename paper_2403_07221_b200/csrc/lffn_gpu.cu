@@ -174,29 +174,42 @@ int launch_hash(lffn_ctx* c, const float* d_x, int64_t n, uint32_t* codes, float
     ++c->launches;
     p.z_in = c->d_zbuf;
   }
-  const int loge = c->logD >= 4 ? 4 : int(c->logD);
+  int loge = c->logD >= kMaxLogE ? kMaxLogE : int(c->logD);
+  if (const char* ov = getenv("LFFN_HASH_LOGE")) {  // tuning override
+    const int o = atoi(ov);
+    if (o >= 1 && o < loge && (c->D >> o) <= 256) loge = o;
+  }
   const int E = 1 << loge;
-  const int tpt = int(c->D / E);
-  const int block = std::max(tpt, std::min(256, int(256 / tpt) * tpt));
+  const int tpt = int(c->D / E);  // <= 256 for D <= 16384
+  const int block = std::max(tpt, (256 / tpt) * tpt);
   const int tpb = block / tpt;
   p.tokens_per_block = tpb;
   p.threads_per_token = tpt;
-  const size_t smem = size_t(tpb) * size_t(c->D + (c->D >> 4)) * sizeof(double);
+  const size_t smem = size_t(tpb) * size_t(padded_len(int(c->D))) * sizeof(double);
   const unsigned grid = (unsigned)((n + tpb - 1) / tpb);
-  switch (loge) {
-#define LFFN_HASH_CASE(L)                                                                  \
-  case L:                                                                                  \
-    cudaFuncSetAttribute(hash_structured_kernel<L>,                                        \
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));          \
-    hash_structured_kernel<L><<<grid, block, smem, st>>>(p);                               \
+  const int kind = c->proj.kind == LFFN_PROJ_SIGNFLIP ? kPreSign
+                   : c->proj.kind == LFFN_PROJ_ACDC   ? kPreDiag
+                                                      : kPreNone;
+  auto go = [&](auto kernel) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    kernel<<<grid, block, smem, st>>>(p);
+  };
+#define LFFN_HASH_CASE(L)                                              \
+  case L:                                                              \
+    if (kind == kPreSign) go(hash_structured_kernel<L, kPreSign>);     \
+    else if (kind == kPreDiag) go(hash_structured_kernel<L, kPreDiag>); \
+    else go(hash_structured_kernel<L, kPreNone>);                      \
     break;
+  switch (loge) {
     LFFN_HASH_CASE(0)
     LFFN_HASH_CASE(1)
     LFFN_HASH_CASE(2)
     LFFN_HASH_CASE(3)
     LFFN_HASH_CASE(4)
-#undef LFFN_HASH_CASE
+    LFFN_HASH_CASE(5)
+    LFFN_HASH_CASE(6)
   }
+#undef LFFN_HASH_CASE
   ++c->launches;
   LFFN_CUDA(cudaGetLastError());
   return LFFN_OK;
@@ -229,9 +242,33 @@ int launch_gather(lffn_ctx* c, const uint32_t* codes, const float* coeff, int64_
       return LFFN_OK;
     }
   }
-  constexpr int NTOK = 4;
   const bool f32 = c->t_dtype == LFFN_F32;
   const int vec = f32 ? ((p.d_out % 4 == 0) ? 4 : 1) : ((p.d_out % 8 == 0) ? 8 : 1);
+  if (vec > 1) {
+    // row-per-warp kernel: MAXC chunks of 32*vec columns per warp
+    const int nchunks = (p.d_out + 32 * vec - 1) / (32 * vec);
+    const int maxc = nchunks <= 2 ? 2 : nchunks <= 4 ? 4 : nchunks <= 6 ? 6 : 8;
+    const int wpt = (nchunks + maxc - 1) / maxc;
+    const bool rec4 = (p.h_loc % 4 == 0) && (reinterpret_cast<uintptr_t>(codes) % 16 == 0) &&
+                      (reinterpret_cast<uintptr_t>(coeff) % 16 == 0);
+    const int64_t warps = n * wpt;
+    const unsigned grid = (unsigned)((warps * 32 + 255) / 256);
+#define LFFN_ROW(TT, V, M)                                                               \
+  if (rec4) gather_row_kernel<TT, V, M, true><<<grid, 256, 0, st>>>(p, wpt);             \
+  else gather_row_kernel<TT, V, M, false><<<grid, 256, 0, st>>>(p, wpt);
+    if (f32) {
+      if (maxc == 2) { LFFN_ROW(float, 4, 2) } else if (maxc == 4) { LFFN_ROW(float, 4, 4) }
+      else if (maxc == 6) { LFFN_ROW(float, 4, 6) } else { LFFN_ROW(float, 4, 8) }
+    } else {
+      if (maxc == 2) { LFFN_ROW(__nv_bfloat16, 8, 2) } else if (maxc == 4) { LFFN_ROW(__nv_bfloat16, 8, 4) }
+      else if (maxc == 6) { LFFN_ROW(__nv_bfloat16, 8, 6) } else { LFFN_ROW(__nv_bfloat16, 8, 8) }
+    }
+#undef LFFN_ROW
+    ++c->launches;
+    LFFN_CUDA(cudaGetLastError());
+    return LFFN_OK;
+  }
+  constexpr int NTOK = 4;
   const int64_t chunks = (p.d_out + 32 * vec - 1) / (32 * vec);
   const int64_t warps = ((n + NTOK - 1) / NTOK) * chunks;
   const unsigned grid = (unsigned)((warps * 32 + 255) / 256);
