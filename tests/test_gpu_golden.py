@@ -1,0 +1,54 @@
+"""The CUDA path against the fixtures generated from the reference itself
+(tests/golden/).  This is the parity check that needs no reference checkout:
+the fixtures travel with the repo to the GPU box."""
+import glob
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+from gpu_helpers import assert_close, device_forward, device_hash
+from paper_2403_07221_b200 import (HashTables, LookupConfig, LookupFFN, LookupVariant, Projection,
+                                   ProjectionSpec, ProjKind, fill_gaussian)
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
+
+
+def build(path):
+    d = dict(np.load(path))
+    cfg = LookupConfig(int(d["d_in"]), int(d["d_out"]), int(d["tables"]), int(d["code_bits"]),
+                       LookupVariant(int(d["variant"])), int(d["neighbor_count"]))
+    spec = ProjectionSpec(cfg.d_in, cfg.code_width(), ProjKind(int(d["kind"])), int(d["stages"]),
+                          int(d["block"]), int(d["depth"]))
+    if "T" in d:
+        T = d["T"]
+    else:
+        T = fill_gaussian(int(d["t_seed"]), cfg.tables * cfg.table_rows() * cfg.d_out,
+                          float(d["t_std"]))
+        assert hashlib.sha256(T.tobytes()).hexdigest() == str(d["tables_sha256"])
+    return d, cfg, Projection.from_blob(spec, d["blob"]), HashTables(cfg.tables, cfg.code_bits,
+                                                                     cfg.d_out, T)
+
+
+DEVICE_CASES = [p for p in GOLDEN
+                if int(np.load(p)["neighbor_count"]) == 1 and int(np.load(p)["kind"]) != 1]
+
+
+@pytest.mark.parametrize("path", DEVICE_CASES, ids=lambda p: os.path.basename(p)[:-4])
+def test_device_matches_reference_fixture(path):
+    d, cfg, proj, T = build(path)
+    x = d["x"].astype(np.float32)
+    assert np.array_equal(x.astype(np.float64), d["x"])  # fixture inputs are fp32 values
+    layer = LookupFFN(cfg, proj, T, max_tokens=x.shape[0])
+    codes, coeff, z = device_hash(layer, x)
+    assert np.array_equal(z.view(np.uint64), d["z"].view(np.uint64)), "z vs reference"
+    assert np.array_equal(codes, d["codes"][..., 0])
+    expect = d["weights"][..., 0]
+    if cfg.scaled_numerator():
+        expect = expect * d["dots"][..., 0]
+    np.testing.assert_allclose(coeff, expect.astype(np.float32), rtol=2.5e-7)
+    y = device_forward(layer, x)
+    assert_close(y, d["y"], 1e-5, os.path.basename(path))
