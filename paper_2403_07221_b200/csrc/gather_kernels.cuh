@@ -19,12 +19,13 @@
 namespace lffn_gpu {
 
 struct GatherParams {
-  const void* T;            // [h_loc][R][d_out] in f32 or bf16
-  const uint32_t* codes;    // [n x h_loc]
-  const float* coeff;       // [n x h_loc]
+  const void* T;            // first table of this launch: [nk][R][d_out], f32 or bf16
+  const uint32_t* codes;    // [n x ld], column 0 = first table of this launch
+  const float* coeff;       // [n x ld]
   float* y;                 // [n x d_out]
   int64_t n;
-  int h_loc;
+  int ld;                   // row stride of codes / coeff (tables owned by the ctx)
+  int nk;                   // tables accumulated by this launch
   int rows;                 // R = 2^tau
   int d_out;
   int accumulate;
@@ -88,11 +89,11 @@ __global__ void __launch_bounds__(256) gather_direct_kernel(GatherParams p) {
 #pragma unroll
     for (int v = 0; v < VEC; ++v) acc[t][v] = 0.f;
 
-  const uint32_t* cbase = p.codes + i0 * p.h_loc;
-  const float* wbase = p.coeff + i0 * p.h_loc;
+  const uint32_t* cbase = p.codes + i0 * p.ld;
+  const float* wbase = p.coeff + i0 * p.ld;
   const int ntok = (p.n - i0) < NTOK ? (int)(p.n - i0) : NTOK;
 
-  for (int k = 0; k < p.h_loc; ++k) {
+  for (int k = 0; k < p.nk; ++k) {
     float vals[NTOK][VEC];
     float w[NTOK];
 #pragma unroll
@@ -101,8 +102,8 @@ __global__ void __launch_bounds__(256) gather_direct_kernel(GatherParams p) {
 #pragma unroll
       for (int v = 0; v < VEC; ++v) vals[t][v] = 0.f;
       if (t < ntok) {
-        const uint32_t code = __ldg(cbase + (int64_t)t * p.h_loc + k);
-        w[t] = __ldg(wbase + (int64_t)t * p.h_loc + k);
+        const uint32_t code = __ldg(cbase + (int64_t)t * p.ld + k);
+        w[t] = __ldg(wbase + (int64_t)t * p.ld + k);
         if (colok) RowLoad<TT, VEC>::load(T + k * table_stride + (int64_t)code * p.d_out + col, vals[t]);
       }
     }
@@ -150,8 +151,8 @@ __global__ void __launch_bounds__(256) gather_row_kernel(GatherParams p, int war
   const int colbase = c0 * CHUNK + lane * VEC;
   const TT* T = reinterpret_cast<const TT*>(p.T);
   const int64_t tstride = (int64_t)p.rows * p.d_out;
-  const uint32_t* cr = p.codes + token * p.h_loc;
-  const float* wr = p.coeff + token * p.h_loc;
+  const uint32_t* cr = p.codes + token * p.ld;
+  const float* wr = p.coeff + token * p.ld;
 
   float acc[MAXC][VEC];
 #pragma unroll
@@ -181,10 +182,10 @@ __global__ void __launch_bounds__(256) gather_row_kernel(GatherParams p, int war
     // records of 4 tables per 128-bit broadcast load
     uint4 cc = __ldg(reinterpret_cast<const uint4*>(cr));
     float4 ww = __ldg(reinterpret_cast<const float4*>(wr));
-    for (int kg = 0; kg < p.h_loc; kg += 4) {
+    for (int kg = 0; kg < p.nk; kg += 4) {
       uint4 cn = cc;
       float4 wn = ww;
-      if (kg + 4 < p.h_loc) {
+      if (kg + 4 < p.nk) {
         cn = __ldg(reinterpret_cast<const uint4*>(cr + kg + 4));
         wn = __ldg(reinterpret_cast<const float4*>(wr + kg + 4));
       }
@@ -203,10 +204,10 @@ __global__ void __launch_bounds__(256) gather_row_kernel(GatherParams p, int war
   } else {
     uint32_t cc = __ldg(cr);
     float ww = __ldg(wr);
-    for (int k = 0; k < p.h_loc; ++k) {
+    for (int k = 0; k < p.nk; ++k) {
       uint32_t cn = cc;
       float wn = ww;
-      if (k + 1 < p.h_loc) {
+      if (k + 1 < p.nk) {
         cn = __ldg(cr + k + 1);
         wn = __ldg(wr + k + 1);
       }
@@ -236,6 +237,93 @@ __global__ void __launch_bounds__(256) gather_row_kernel(GatherParams p, int war
       } else {
 #pragma unroll
         for (int v = 0; v < VEC; ++v) yr[col + v] = acc[c][v];
+      }
+    }
+  }
+  if (bad) atomicOr(p.flag, bad);
+}
+
+// Persistent variant of the row kernel (REC4 records only): the grid covers
+// the SMs once and every warp walks tokens with a grid stride, TIF tables'
+// rows in flight per lane, MINB blocks per SM requested from ptxas.
+template <typename TT, int VEC, int MAXC, int TIF, int MINB>
+__global__ void __launch_bounds__(256, MINB) gather_row_persistent_kernel(GatherParams p,
+                                                                          int warps_per_token) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  constexpr int CHUNK = 32 * VEC;
+  const int nchunks = (p.d_out + CHUNK - 1) / CHUNK;
+  const TT* T = reinterpret_cast<const TT*>(p.T);
+  const int64_t tstride = (int64_t)p.rows * p.d_out;
+  int bad = 0;
+  for (int64_t item = gwarp; item < p.n * warps_per_token; item += nwarps) {
+    const int64_t token = item / warps_per_token;
+    const int part = (int)(item - token * warps_per_token);
+    const int c0 = part * MAXC;
+    const int nck = min(MAXC, nchunks - c0);
+    const int colbase = c0 * CHUNK + lane * VEC;
+    const uint32_t* cr = p.codes + token * p.ld;
+    const float* wr = p.coeff + token * p.ld;
+    float acc[MAXC][VEC];
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c)
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) acc[c][v] = 0.f;
+    uint4 cc = __ldg(reinterpret_cast<const uint4*>(cr));
+    float4 ww = __ldg(reinterpret_cast<const float4*>(wr));
+    for (int kg = 0; kg < p.nk; kg += 4) {
+      uint4 cn = cc;
+      float4 wn = ww;
+      if (kg + 4 < p.nk) {
+        cn = __ldg(reinterpret_cast<const uint4*>(cr + kg + 4));
+        wn = __ldg(reinterpret_cast<const float4*>(wr + kg + 4));
+      }
+      const uint32_t codes4[4] = {cc.x, cc.y, cc.z, cc.w};
+      const float w4[4] = {ww.x, ww.y, ww.z, ww.w};
+#pragma unroll
+      for (int q0 = 0; q0 < 4; q0 += TIF) {
+        float vals[TIF][MAXC][VEC];
+#pragma unroll
+        for (int q = 0; q < TIF; ++q) {
+          const TT* rp = T + (kg + q0 + q) * tstride + (int64_t)codes4[q0 + q] * p.d_out + colbase;
+#pragma unroll
+          for (int c = 0; c < MAXC; ++c) {
+            if (c < nck && colbase + c * CHUNK < p.d_out) RowLoad<TT, VEC>::load(rp + c * CHUNK, vals[q][c]);
+            else {
+#pragma unroll
+              for (int v = 0; v < VEC; ++v) vals[q][c][v] = 0.f;
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < TIF; ++q)
+#pragma unroll
+          for (int c = 0; c < MAXC; ++c)
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) acc[c][v] = fmaf(w4[q0 + q], vals[q][c][v], acc[c][v]);
+      }
+      cc = cn;
+      ww = wn;
+    }
+    float* yr = p.y + token * p.d_out;
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+      const int col = colbase + c * CHUNK;
+      if (c < nck && col < p.d_out) {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+          float o = acc[c][v];
+          if (p.accumulate) o += yr[col + v];
+          if (!isfinite(o)) bad = 4;
+          acc[c][v] = o;
+        }
+        if constexpr (VEC == 4) {
+          *reinterpret_cast<float4*>(yr + col) = make_float4(acc[c][0], acc[c][1], acc[c][2], acc[c][3]);
+        } else {
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) yr[col + v] = acc[c][v];
+        }
       }
     }
   }

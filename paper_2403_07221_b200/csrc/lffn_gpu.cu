@@ -76,6 +76,8 @@ struct lffn_ctx {
   int64_t launches = 0;
   int staged_ok = 0;
   int staged_smem = 0;
+  int num_sms = 148;
+  size_t table_group_bytes = 0;  // >0: walk tables in groups of this many bytes (measured slower on c2)
 };
 
 namespace {
@@ -215,25 +217,22 @@ int launch_hash(lffn_ctx* c, const float* d_x, int64_t n, uint32_t* codes, float
   return LFFN_OK;
 }
 
-int launch_gather(lffn_ctx* c, const uint32_t* codes, const float* coeff, int64_t n, float* y,
-                  int accumulate, cudaStream_t st) {
-  if (n == 0) return LFFN_OK;
-  if (!c->d_T) return fail(LFFN_ERR_USAGE, "lookup forward: tables not uploaded");
+// One gather launch over tables [k0, k0 + nk) of the context's slice.
+int launch_gather_group(lffn_ctx* c, const uint32_t* codes, const float* coeff, int64_t n,
+                        float* y, int accumulate, int64_t k0, int64_t nk, cudaStream_t st) {
   GatherParams p{};
-  p.T = c->d_T;
-  p.codes = codes;
-  p.coeff = coeff;
+  const size_t esz = c->t_dtype == LFFN_F32 ? 4 : 2;
+  p.T = static_cast<const char*>(c->d_T) + size_t(k0) * size_t(c->rows) * size_t(c->cfg.d_out) * esz;
+  p.codes = codes + k0;
+  p.coeff = coeff + k0;
   p.y = y;
   p.n = n;
-  p.h_loc = int(c->h_loc);
+  p.ld = int(c->h_loc);
+  p.nk = int(nk);
   p.rows = int(c->rows);
   p.d_out = int(c->cfg.d_out);
   p.accumulate = accumulate;
   p.flag = c->d_flag;
-  if (c->h_loc == 0) {
-    if (!accumulate) LFFN_CUDA(cudaMemsetAsync(y, 0, size_t(n) * p.d_out * sizeof(float), st));
-    return LFFN_OK;
-  }
   if (staged_gather_applicable(c->staged_ok, p, c->t_dtype)) {
     int rc = launch_staged_gather(p, c->t_dtype, c->staged_smem, st);
     ++c->launches;
@@ -247,21 +246,38 @@ int launch_gather(lffn_ctx* c, const uint32_t* codes, const float* coeff, int64_
   if (vec > 1) {
     // row-per-warp kernel: MAXC chunks of 32*vec columns per warp
     const int nchunks = (p.d_out + 32 * vec - 1) / (32 * vec);
-    const int maxc = nchunks <= 2 ? 2 : nchunks <= 4 ? 4 : nchunks <= 6 ? 6 : 8;
+    // chunks per warp: register budget of the persistent kernel (no spills)
+    const int maxc = nchunks <= 2 ? 2 : (nchunks <= 4 || !f32) ? 4 : (nchunks <= 6 ? 6 : 4);
     const int wpt = (nchunks + maxc - 1) / maxc;
-    const bool rec4 = (p.h_loc % 4 == 0) && (reinterpret_cast<uintptr_t>(codes) % 16 == 0) &&
-                      (reinterpret_cast<uintptr_t>(coeff) % 16 == 0);
+    const bool rec4 = (p.ld % 4 == 0) && (p.nk % 4 == 0) &&
+                      (reinterpret_cast<uintptr_t>(p.codes) % 16 == 0) &&
+                      (reinterpret_cast<uintptr_t>(p.coeff) % 16 == 0);
     const int64_t warps = n * wpt;
     const unsigned grid = (unsigned)((warps * 32 + 255) / 256);
+    if (rec4) {
+      // persistent row kernel: grid = 2 CTAs per SM, 4 (f32) / 2 (bf16)
+      // tables' rows in flight per lane
+      const unsigned pg = (unsigned)std::min<int64_t>(int64_t(c->num_sms) * 2, (warps * 32 + 255) / 256);
+#define LFFN_PROW(TT, V, M, TIF) gather_row_persistent_kernel<TT, V, M, TIF, 2><<<pg, 256, 0, st>>>(p, wpt);
+      if (f32) {
+        if (maxc == 2) { LFFN_PROW(float, 4, 2, 4) } else if (maxc == 4) { LFFN_PROW(float, 4, 4, 4) }
+        else { LFFN_PROW(float, 4, 6, 4) }
+      } else {
+        if (maxc == 2) { LFFN_PROW(__nv_bfloat16, 8, 2, 4) } else { LFFN_PROW(__nv_bfloat16, 8, 4, 2) }
+      }
+#undef LFFN_PROW
+      ++c->launches;
+      LFFN_CUDA(cudaGetLastError());
+      return LFFN_OK;
+    }
 #define LFFN_ROW(TT, V, M)                                                               \
   if (rec4) gather_row_kernel<TT, V, M, true><<<grid, 256, 0, st>>>(p, wpt);             \
   else gather_row_kernel<TT, V, M, false><<<grid, 256, 0, st>>>(p, wpt);
     if (f32) {
       if (maxc == 2) { LFFN_ROW(float, 4, 2) } else if (maxc == 4) { LFFN_ROW(float, 4, 4) }
-      else if (maxc == 6) { LFFN_ROW(float, 4, 6) } else { LFFN_ROW(float, 4, 8) }
+      else { LFFN_ROW(float, 4, 6) }
     } else {
-      if (maxc == 2) { LFFN_ROW(__nv_bfloat16, 8, 2) } else if (maxc == 4) { LFFN_ROW(__nv_bfloat16, 8, 4) }
-      else if (maxc == 6) { LFFN_ROW(__nv_bfloat16, 8, 6) } else { LFFN_ROW(__nv_bfloat16, 8, 8) }
+      if (maxc == 2) { LFFN_ROW(__nv_bfloat16, 8, 2) } else { LFFN_ROW(__nv_bfloat16, 8, 4) }
     }
 #undef LFFN_ROW
     ++c->launches;
@@ -278,6 +294,37 @@ int launch_gather(lffn_ctx* c, const uint32_t* codes, const float* coeff, int64_
   else gather_direct_kernel<__nv_bfloat16, 1, NTOK><<<grid, 256, 0, st>>>(p);
   ++c->launches;
   LFFN_CUDA(cudaGetLastError());
+  return LFFN_OK;
+}
+
+// Tables larger than L2 are walked in groups of at most ~table_group_bytes
+// (all tokens finish group g before group g+1 starts), so each table row is
+// fetched from HBM about once per forward instead of once per wave of
+// resident tokens; y is accumulated across groups (it stays L2-resident).
+int launch_gather(lffn_ctx* c, const uint32_t* codes, const float* coeff, int64_t n, float* y,
+                  int accumulate, cudaStream_t st) {
+  if (n == 0) return LFFN_OK;
+  if (!c->d_T) return fail(LFFN_ERR_USAGE, "lookup forward: tables not uploaded");
+  if (c->h_loc == 0) {
+    if (!accumulate)
+      LFFN_CUDA(cudaMemsetAsync(y, 0, size_t(n) * size_t(c->cfg.d_out) * sizeof(float), st));
+    return LFFN_OK;
+  }
+  const size_t esz = c->t_dtype == LFFN_F32 ? 4 : 2;
+  const size_t table_bytes = size_t(c->rows) * size_t(c->cfg.d_out) * esz;
+  int64_t per = c->h_loc;
+  if (c->table_group_bytes > 0 && table_bytes * size_t(c->h_loc) > c->table_group_bytes) {
+    per = std::max<int64_t>(1, int64_t(c->table_group_bytes / table_bytes));
+    if (per >= 4) per &= ~int64_t(3);  // keep the 4-table record loads
+    const int64_t groups = (c->h_loc + per - 1) / per;
+    per = (c->h_loc + groups - 1) / groups;  // balance the groups
+    if (per >= 4) per = (per + 3) & ~int64_t(3);
+  }
+  for (int64_t k0 = 0; k0 < c->h_loc; k0 += per) {
+    const int64_t nk = std::min(per, c->h_loc - k0);
+    if (int rc = launch_gather_group(c, codes, coeff, n, y, (k0 > 0) ? 1 : accumulate, k0, nk, st))
+      return rc;
+  }
   return LFFN_OK;
 }
 
@@ -441,6 +488,8 @@ int lffn_ctx_create_shard(lffn_ctx** out, int device, int64_t max_tokens, const 
   CK(cudaEventCreate(&c->ev_t1));
   CK(cudaEventCreate(&c->ev_t2));
   c->staged_ok = staged_gather_configure(int(c->rows), int(cfg->d_out), &c->staged_smem);
+  c->num_sms = prop.multiProcessorCount;
+  if (const char* g = getenv("LFFN_TABLE_GROUP_MB")) c->table_group_bytes = size_t(atol(g)) << 20;
 #undef CK
   *out = c;
   return LFFN_OK;

@@ -1,0 +1,116 @@
+#!/usr/bin/env python
+"""Summarise ncu output for profiles/.
+
+    python tools/ncu_summary.py launches gpurun_out/launches.csv   > profiles/<round>_launches.md
+    python tools/ncu_summary.py full gpurun_out/prof.ncu-rep        > profiles/<round>_ncu_full.md
+    python tools/ncu_summary.py traffic gpurun_out/prof.ncu-rep KEY  (prints JSON for profiles/ncu_gather_traffic.json)
+"""
+from __future__ import annotations
+
+import collections
+import csv
+import io
+import json
+import subprocess
+import sys
+
+FULL_METRICS = [
+    ("gpu__time_duration.sum", "duration"),
+    ("dram__bytes_read.sum", "dram read"),
+    ("dram__bytes_write.sum", "dram write"),
+    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "dram % peak"),
+    ("lts__t_bytes.sum", "L2 bytes"),
+    ("lts__t_bytes.sum.per_second", "L2 bytes/s"),
+    ("lts__t_sector_hit_rate.pct", "L2 hit %"),
+    ("l1tex__t_bytes.sum", "L1 bytes"),
+    ("l1tex__t_sector_hit_rate.pct", "L1 hit %"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smem wavefronts"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
+    ("launch__registers_per_thread", "regs/thread"),
+    ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "fp64 pipe %"),
+    ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput %"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
+]
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    # ncu --csv --log-file: header row contains "Kernel Name" and "Metric Value"
+    hdr_i = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    hdr = rows[hdr_i]
+    ki, mi, vi, ui = (hdr.index("Kernel Name"), hdr.index("Metric Name"),
+                      hdr.index("Metric Value"), hdr.index("Metric Unit"))
+    agg = collections.OrderedDict()
+    for r in rows[hdr_i + 1:]:
+        if len(r) <= vi or r[mi] != "gpu__time_duration.sum":
+            continue
+        v = float(r[vi].replace(",", ""))
+        unit = r[ui]
+        us = v / 1000.0 if unit == "nsecond" else v * (1000.0 if unit == "msecond" else 1.0)
+        name = r[ki].split("(")[0]
+        a = agg.setdefault(name, [0, 0.0])
+        a[0] += 1
+        a[1] += us
+    total = sum(v[1] for v in agg.values())
+    print("| kernel | launches | total us | avg us | share |")
+    print("|---|---:|---:|---:|---:|")
+    for name, (cnt, us) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+        print(f"| `{name}` | {cnt} | {us:.1f} | {us / cnt:.1f} | {100 * us / total:.1f}% |")
+    print(f"\nTotal device time of listed launches: {total:.1f} us "
+          "(cold-cache, serialised under ncu: compare shares, not absolutes).")
+
+
+def raw(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    return hdr, units, rows[2:]
+
+
+def stalls(hdr, row):
+    items = []
+    for i, h in enumerate(hdr):
+        if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("not_issued"):
+            try:
+                v = float(row[i].replace(",", ""))
+            except ValueError:
+                continue
+            if v > 0:
+                items.append((v, h.replace("smsp__pcsamp_warps_issue_stalled_", "")))
+    items.sort(reverse=True)
+    tot = sum(v for v, _ in items) or 1.0
+    return ", ".join(f"{n} {100 * v / tot:.0f}%" for v, n in items[:6])
+
+
+def full(path):
+    hdr, units, rows = raw(path)
+    ki = hdr.index("Kernel Name")
+    for row in rows:
+        print(f"### `{row[ki][:120]}`\n")
+        print("| metric | value |")
+        print("|---|---:|")
+        for m, label in FULL_METRICS:
+            if m in hdr:
+                i = hdr.index(m)
+                print(f"| {label} (`{m}`) | {row[i]} {units[i]} |")
+        print(f"| top stall reasons | {stalls(hdr, row)} |\n")
+
+
+def traffic(path, key):
+    hdr, units, rows = raw(path)
+    ki = hdr.index("Kernel Name")
+    for row in rows:
+        if "gather" in row[ki]:
+            rd = float(row[hdr.index("dram__bytes_read.sum")].replace(",", ""))
+            wr = float(row[hdr.index("dram__bytes_write.sum")].replace(",", ""))
+            ur = units[hdr.index("dram__bytes_read.sum")]
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(ur, 1)
+            print(json.dumps({key: {"dram_bytes_per_launch": (rd + wr) * scale,
+                                    "source": path}}))
+            return
+
+
+if __name__ == "__main__":
+    {"launches": lambda: launches(sys.argv[2]), "full": lambda: full(sys.argv[2]),
+     "traffic": lambda: traffic(sys.argv[2], sys.argv[3])}[sys.argv[1]]()
