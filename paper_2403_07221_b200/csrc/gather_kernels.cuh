@@ -243,12 +243,43 @@ __global__ void __launch_bounds__(256) gather_row_kernel(GatherParams p, int war
   if (bad) atomicOr(p.flag, bad);
 }
 
-// Persistent variant of the row kernel (REC4 records only): the grid covers
-// the SMs once and every warp walks tokens with a grid stride, TIF tables'
-// rows in flight per lane, MINB blocks per SM requested from ptxas.
-template <typename TT, int VEC, int MAXC, int TIF, int MINB>
+// 128-bit raw row segment: kept packed while in flight (4 registers for 4
+// fp32 or 8 bf16 values) and widened to fp32 only at the FMA.
+template <typename TT>
+struct Raw {
+  static constexpr int VEC = sizeof(uint4) / sizeof(TT);
+  static __device__ __forceinline__ uint4 load(const TT* p) {
+    return __ldg(reinterpret_cast<const uint4*>(p));
+  }
+  static __device__ __forceinline__ void fma(float (&acc)[VEC], float w, const uint4& r) {
+    if constexpr (VEC == 4) {
+      acc[0] = fmaf(w, __uint_as_float(r.x), acc[0]);
+      acc[1] = fmaf(w, __uint_as_float(r.y), acc[1]);
+      acc[2] = fmaf(w, __uint_as_float(r.z), acc[2]);
+      acc[3] = fmaf(w, __uint_as_float(r.w), acc[3]);
+    } else {
+      acc[0] = fmaf(w, bf16lo(r.x), acc[0]);
+      acc[1] = fmaf(w, bf16hi(r.x), acc[1]);
+      acc[2] = fmaf(w, bf16lo(r.y), acc[2]);
+      acc[3] = fmaf(w, bf16hi(r.y), acc[3]);
+      acc[4] = fmaf(w, bf16lo(r.z), acc[4]);
+      acc[5] = fmaf(w, bf16hi(r.z), acc[5]);
+      acc[6] = fmaf(w, bf16lo(r.w), acc[6]);
+      acc[7] = fmaf(w, bf16hi(r.w), acc[7]);
+    }
+  }
+};
+
+// Persistent row kernel (the default): one warp per (token, part of its
+// row), the grid covers the SMs MINB CTAs deep and walks tokens with a grid
+// stride, and every lane keeps TIF tables' 128-bit row segments in flight
+// (packed) while the (code, coeff) records of the next four tables are
+// prefetched.  Requires the 4-table record layout (nk % 4 == 0, ld % 4 == 0,
+// 16-byte aligned record pointers); 16-byte aligned rows (d_out % VEC == 0).
+template <typename TT, int MAXC, int TIF, int MINB>
 __global__ void __launch_bounds__(256, MINB) gather_row_persistent_kernel(GatherParams p,
                                                                           int warps_per_token) {
+  constexpr int VEC = Raw<TT>::VEC;
   const int lane = threadIdx.x & 31;
   const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -261,8 +292,10 @@ __global__ void __launch_bounds__(256, MINB) gather_row_persistent_kernel(Gather
     const int64_t token = item / warps_per_token;
     const int part = (int)(item - token * warps_per_token);
     const int c0 = part * MAXC;
-    const int nck = min(MAXC, nchunks - c0);
     const int colbase = c0 * CHUNK + lane * VEC;
+    bool ok[MAXC];
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) ok[c] = (c0 + c < nchunks) && (colbase + c * CHUNK < p.d_out);
     const uint32_t* cr = p.codes + token * p.ld;
     const float* wr = p.coeff + token * p.ld;
     float acc[MAXC][VEC];
@@ -283,25 +316,18 @@ __global__ void __launch_bounds__(256, MINB) gather_row_persistent_kernel(Gather
       const float w4[4] = {ww.x, ww.y, ww.z, ww.w};
 #pragma unroll
       for (int q0 = 0; q0 < 4; q0 += TIF) {
-        float vals[TIF][MAXC][VEC];
+        uint4 raw[TIF][MAXC];
 #pragma unroll
         for (int q = 0; q < TIF; ++q) {
           const TT* rp = T + (kg + q0 + q) * tstride + (int64_t)codes4[q0 + q] * p.d_out + colbase;
 #pragma unroll
-          for (int c = 0; c < MAXC; ++c) {
-            if (c < nck && colbase + c * CHUNK < p.d_out) RowLoad<TT, VEC>::load(rp + c * CHUNK, vals[q][c]);
-            else {
-#pragma unroll
-              for (int v = 0; v < VEC; ++v) vals[q][c][v] = 0.f;
-            }
-          }
+          for (int c = 0; c < MAXC; ++c)
+            raw[q][c] = ok[c] ? Raw<TT>::load(rp + c * CHUNK) : make_uint4(0u, 0u, 0u, 0u);
         }
 #pragma unroll
         for (int q = 0; q < TIF; ++q)
 #pragma unroll
-          for (int c = 0; c < MAXC; ++c)
-#pragma unroll
-            for (int v = 0; v < VEC; ++v) acc[c][v] = fmaf(w4[q0 + q], vals[q][c][v], acc[c][v]);
+          for (int c = 0; c < MAXC; ++c) Raw<TT>::fma(acc[c], w4[q0 + q], raw[q][c]);
       }
       cc = cn;
       ww = wn;
@@ -309,22 +335,19 @@ __global__ void __launch_bounds__(256, MINB) gather_row_persistent_kernel(Gather
     float* yr = p.y + token * p.d_out;
 #pragma unroll
     for (int c = 0; c < MAXC; ++c) {
+      if (!ok[c]) continue;
       const int col = colbase + c * CHUNK;
-      if (c < nck && col < p.d_out) {
 #pragma unroll
-        for (int v = 0; v < VEC; ++v) {
-          float o = acc[c][v];
-          if (p.accumulate) o += yr[col + v];
-          if (!isfinite(o)) bad = 4;
-          acc[c][v] = o;
-        }
-        if constexpr (VEC == 4) {
-          *reinterpret_cast<float4*>(yr + col) = make_float4(acc[c][0], acc[c][1], acc[c][2], acc[c][3]);
-        } else {
-#pragma unroll
-          for (int v = 0; v < VEC; ++v) yr[col + v] = acc[c][v];
-        }
+      for (int v = 0; v < VEC; ++v) {
+        float o = acc[c][v];
+        if (p.accumulate) o += yr[col + v];
+        if (!isfinite(o)) bad = 4;
+        acc[c][v] = o;
       }
+#pragma unroll
+      for (int v = 0; v < VEC; v += 4)
+        *reinterpret_cast<float4*>(yr + col + v) =
+            make_float4(acc[c][v], acc[c][v + 1], acc[c][v + 2], acc[c][v + 3]);
     }
   }
   if (bad) atomicOr(p.flag, bad);

@@ -168,7 +168,7 @@ enum : int { kPreNone = 0, kPreSign = 1, kPreDiag = 2 };
 // before a transform (signflip sign flip / acdc diagonal), phase 0 only.
 template <int LOGE, int B, bool SRC_X, int PRE>
 __device__ __forceinline__ void phase_smem(double* sm, int t, int tpt, int lo, const HashParams& p,
-                                           int tr, const float* xr, int& bad) {
+                                           int tr, const float* xr, int& bad, bool last) {
   constexpr int E = 1 << LOGE;
   constexpr int G = 1 << B;
   double v[E];
@@ -217,27 +217,60 @@ __device__ __forceinline__ void phase_smem(double* sm, int t, int tpt, int lo, c
     for (int r = 0; r < E; ++r) v[r] = __dmul_rn(v[r], __ldg(dg + r));
   }
   butterfly_groups<LOGE, B>(v);
+  if (last && p.code_width == p.D) {
+    // finiteness of the projection output (projection.cpp:264,
+    // lookup.cpp:204) on the registers: some exponent field all ones
+    uint32_t m = 0xffffffffu;
+#pragma unroll
+    for (int r = 0; r < E; ++r) m = min(m, (uint32_t)(__double2hiint(v[r]) & 0x7ff00000) ^ 0x7ff00000u);
+    if (m == 0u) bad |= 2;
+  }
   phase_io<LOGE, B, true>(sm, v, t, lo);
 }
 
 // Phase 0 of transform tr (bits [0, LOGE)) -- the pre-factor phase.
 template <int LOGE, int PRE>
 __device__ __forceinline__ void run_first_phase(double* sm, int t, int tpt, const HashParams& p,
-                                                int tr, const float* xr, int& bad) {
-  if (tr == 0) phase_smem<LOGE, LOGE, true, PRE>(sm, t, tpt, 0, p, tr, xr, bad);
-  else phase_smem<LOGE, LOGE, false, PRE>(sm, t, tpt, 0, p, tr, xr, bad);
+                                                int tr, const float* xr, int& bad, bool last) {
+  if (tr == 0) phase_smem<LOGE, LOGE, true, PRE>(sm, t, tpt, 0, p, tr, xr, bad, last);
+  else phase_smem<LOGE, LOGE, false, PRE>(sm, t, tpt, 0, p, tr, xr, bad, last);
 }
 
 // Later phases (bits [lo, lo+b), b <= LOGE).
 template <int LOGE>
 __device__ __forceinline__ void run_later_phase(double* sm, int t, int tpt, int lo, int b,
-                                                const HashParams& p, int tr, int& bad) {
-  if constexpr (LOGE >= 6) { if (b == 6) { phase_smem<LOGE, 6, false, kPreNone>(sm, t, tpt, lo, p, tr, nullptr, bad); return; } }
-  if constexpr (LOGE >= 5) { if (b == 5) { phase_smem<LOGE, 5, false, kPreNone>(sm, t, tpt, lo, p, tr, nullptr, bad); return; } }
-  if constexpr (LOGE >= 4) { if (b == 4) { phase_smem<LOGE, 4, false, kPreNone>(sm, t, tpt, lo, p, tr, nullptr, bad); return; } }
-  if constexpr (LOGE >= 3) { if (b == 3) { phase_smem<LOGE, 3, false, kPreNone>(sm, t, tpt, lo, p, tr, nullptr, bad); return; } }
-  if constexpr (LOGE >= 2) { if (b == 2) { phase_smem<LOGE, 2, false, kPreNone>(sm, t, tpt, lo, p, tr, nullptr, bad); return; } }
-  if constexpr (LOGE >= 1) { if (b == 1) { phase_smem<LOGE, 1, false, kPreNone>(sm, t, tpt, lo, p, tr, nullptr, bad); return; } }
+                                                const HashParams& p, int tr, int& bad, bool last) {
+  if constexpr (LOGE >= 6) { if (b == 6) { phase_smem<LOGE, 6, false, kPreNone>(sm, t, tpt, lo, p, tr, nullptr, bad, last); return; } }
+  if constexpr (LOGE >= 5) { if (b == 5) { phase_smem<LOGE, 5, false, kPreNone>(sm, t, tpt, lo, p, tr, nullptr, bad, last); return; } }
+  if constexpr (LOGE >= 4) { if (b == 4) { phase_smem<LOGE, 4, false, kPreNone>(sm, t, tpt, lo, p, tr, nullptr, bad, last); return; } }
+  if constexpr (LOGE >= 3) { if (b == 3) { phase_smem<LOGE, 3, false, kPreNone>(sm, t, tpt, lo, p, tr, nullptr, bad, last); return; } }
+  if constexpr (LOGE >= 2) { if (b == 2) { phase_smem<LOGE, 2, false, kPreNone>(sm, t, tpt, lo, p, tr, nullptr, bad, last); return; } }
+  if constexpr (LOGE >= 1) { if (b == 1) { phase_smem<LOGE, 1, false, kPreNone>(sm, t, tpt, lo, p, tr, nullptr, bad, last); return; } }
+}
+
+// 1 + exp(-2a), kept out of line: it is needed only for |z| < 18.5 (rare
+// for the unnormalised transforms), and inlining it per coordinate bloats
+// the kernel past the instruction cache.
+__device__ __noinline__ double one_plus_exp_m2(double a) { return __dadd_rn(1.0, exp(-2.0 * a)); }
+
+// Phase 0 of transform tr (bits [0, LOGE)) -- the pre-factor phase.
+template <int LOGE, int PRE>
+__device__ __forceinline__ void run_first_phase(double* sm, int t, int tpt, const HashParams& p,
+                                                int tr, const float* xr, int& bad, bool last) {
+  if (tr == 0) phase_smem<LOGE, LOGE, true, PRE>(sm, t, tpt, 0, p, tr, xr, bad, last);
+  else phase_smem<LOGE, LOGE, false, PRE>(sm, t, tpt, 0, p, tr, xr, bad, last);
+}
+
+// Later phases (bits [lo, lo+b), b <= LOGE).
+template <int LOGE>
+__device__ __forceinline__ void run_later_phase(double* sm, int t, int tpt, int lo, int b,
+                                                const HashParams& p, int tr, int& bad, bool last) {
+  if constexpr (LOGE >= 6) { if (b == 6) { phase_smem<LOGE, 6, false, kPreNone>(sm, t, tpt, lo, p, tr, nullptr, bad, last); return; } }
+  if constexpr (LOGE >= 5) { if (b == 5) { phase_smem<LOGE, 5, false, kPreNone>(sm, t, tpt, lo, p, tr, nullptr, bad, last); return; } }
+  if constexpr (LOGE >= 4) { if (b == 4) { phase_smem<LOGE, 4, false, kPreNone>(sm, t, tpt, lo, p, tr, nullptr, bad, last); return; } }
+  if constexpr (LOGE >= 3) { if (b == 3) { phase_smem<LOGE, 3, false, kPreNone>(sm, t, tpt, lo, p, tr, nullptr, bad, last); return; } }
+  if constexpr (LOGE >= 2) { if (b == 2) { phase_smem<LOGE, 2, false, kPreNone>(sm, t, tpt, lo, p, tr, nullptr, bad, last); return; } }
+  if constexpr (LOGE >= 1) { if (b == 1) { phase_smem<LOGE, 1, false, kPreNone>(sm, t, tpt, lo, p, tr, nullptr, bad, last); return; } }
 }
 
 // 1 + exp(-2a), kept out of line: it is needed only for |z| < 18.5 (rare
@@ -269,8 +302,8 @@ __device__ __forceinline__ void code_and_coeff(const double* sm, int base, int t
 // K1 for structured projections (signflip, acdc) and the epilogue of the
 // dense projection (z_in given).
 // KIND: kPreSign (signflip), kPreDiag (acdc), kPreNone (dense epilogue on z_in).
-template <int LOGE, int KIND>
-__global__ void __launch_bounds__(256) hash_structured_kernel(HashParams p) {
+template <int LOGE, int KIND, int NT = 256, int MINB = 1>
+__global__ void __launch_bounds__(NT, MINB) hash_structured_kernel(HashParams p) {
   extern __shared__ double smem[];
   constexpr int E = 1 << LOGE;
   const int tpt = p.threads_per_token;
@@ -299,37 +332,62 @@ __global__ void __launch_bounds__(256) hash_structured_kernel(HashParams p) {
     int nph = 1;
     if constexpr (LOGE > 0) nph = (p.logD + LOGE - 1) / LOGE;
     for (int tr = 0; tr < p.n_transforms; ++tr) {
-      if (active) run_first_phase<LOGE, KIND>(sm, t, tpt, p, tr, xr, bad);
+      const bool last_tr = tr == p.n_transforms - 1;
+      if (active) run_first_phase<LOGE, KIND>(sm, t, tpt, p, tr, xr, bad, last_tr && nph == 1);
       token_sync();
       for (int ph = 1; ph < nph; ++ph) {
         const int lo = ph * LOGE;
-        if (active) run_later_phase<LOGE>(sm, t, tpt, lo, min(LOGE, p.logD - lo), p, tr, bad);
+        if (active)
+          run_later_phase<LOGE>(sm, t, tpt, lo, min(LOGE, p.logD - lo), p, tr, bad,
+                                last_tr && ph == nph - 1);
         token_sync();
       }
     }
   }
 
   if (active) {
-    // finiteness of the whole projection output (projection.cpp:264,
-    // lookup.cpp:204) and the optional z copy-out, coalesced
-    for (int a = t; a < p.code_width; a += tpt) {
-      const double zv = sm[spos(a)];
-      if (!isfinite(zv)) bad |= 2;
-      if (p.z_out) p.z_out[token * p.code_width + a] = zv;
+    if (p.z_out || KIND == kPreNone || p.code_width != p.D) {
+      // finiteness of the first h*tau outputs (projection.cpp:264,
+      // lookup.cpp:204) when the registers did not cover exactly them, and
+      // the optional z copy-out (coalesced)
+      for (int a = t; a < p.code_width; a += tpt) {
+        const double zv = sm[spos(a)];
+        if (!isfinite(zv)) bad |= 2;
+        if (p.z_out) p.z_out[token * p.code_width + a] = zv;
+      }
     }
     // each table is finished by the thread whose element range holds its
-    // first coordinate; with the 65-double stride the sequential reads of
-    // neighbouring threads stay (nearly) bank-conflict free
+    // first coordinate (neighbouring threads read 66 doubles apart: no bank
+    // conflicts)
     const int tau = p.tau;
     const int hl = p.ke - p.kb;
     const int a_lo = t * E;
     const int a_hi = min(a_lo + E, p.code_width);
     for (int k = max((a_lo + tau - 1) / tau, p.kb); k < p.ke && k * tau < a_hi; ++k) {
-      uint32_t code;
-      float cf;
-      code_and_coeff(sm, k * tau, tau, p.scaled, &code, &cf);
+      const int base = k * tau;
+      uint32_t code = 0;
+      bool small = false;
+      double sum_abs = 0.0;
+#pragma unroll 4
+      for (int j = 0; j < tau; ++j) {
+        const double zj = sm[spos(base + j)];
+        code |= (zj >= 0.0 ? 1u : 0u) << j;
+        const double az = fabs(zj);
+        small |= az < 18.5;
+        sum_abs = __dadd_rn(sum_abs, az);
+      }
+      double w = 1.0;
+      if (small) {
+        // 1 + exp(-2a) == 1.0 exactly once exp(-2a) <= 2^-53 (a >= 18.37),
+        // so only coordinates with a < 18.5 divide; same order as the
+        // reference's w /= 1 + exp(-2|z_j|) (lookup.cpp:185-189)
+        for (int j = 0; j < tau; ++j) {
+          const double az = fabs(sm[spos(base + j)]);
+          if (az < 18.5) w = __ddiv_rn(w, one_plus_exp_m2(az));
+        }
+      }
       p.codes[token * hl + (k - p.kb)] = code;
-      p.coeff[token * hl + (k - p.kb)] = cf;
+      p.coeff[token * hl + (k - p.kb)] = (float)(p.scaled ? __dmul_rn(w, sum_abs) : w);
     }
   }
   if (bad) atomicOr(p.flag, bad);

@@ -183,7 +183,11 @@ int launch_hash(lffn_ctx* c, const float* d_x, int64_t n, uint32_t* codes, float
   }
   const int E = 1 << loge;
   const int tpt = int(c->D / E);  // <= 256 for D <= 16384
-  const int block = std::max(tpt, (256 / tpt) * tpt);
+  // LOGE 6 (one warp per D <= 2048 token, ~214 registers): 128-thread CTAs
+  // measured fastest (c2 hash 0.233 ms vs 0.251 ms with 256-thread CTAs)
+  static const int hvar = getenv("LFFN_HASH_VARIANT") ? atoi(getenv("LFFN_HASH_VARIANT")) : 2;
+  const int nt = (hvar > 0 && loge == 6 && tpt <= 128) ? 128 : 256;
+  const int block = std::max(tpt, (nt / tpt) * tpt);
   const int tpb = block / tpt;
   p.tokens_per_block = tpb;
   p.threads_per_token = tpt;
@@ -196,6 +200,14 @@ int launch_hash(lffn_ctx* c, const float* d_x, int64_t n, uint32_t* codes, float
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     kernel<<<grid, block, smem, st>>>(p);
   };
+  if (nt == 128 && kind == kPreSign) {  // tuning variants (LFFN_HASH_VARIANT)
+    if (hvar == 1) go(hash_structured_kernel<6, kPreSign, 128, 3>);
+    else if (hvar == 2) go(hash_structured_kernel<6, kPreSign, 128, 2>);
+    else go(hash_structured_kernel<6, kPreSign, 128, 4>);
+    ++c->launches;
+    LFFN_CUDA(cudaGetLastError());
+    return LFFN_OK;
+  }
 #define LFFN_HASH_CASE(L)                                              \
   case L:                                                              \
     if (kind == kPreSign) go(hash_structured_kernel<L, kPreSign>);     \
@@ -255,15 +267,21 @@ int launch_gather_group(lffn_ctx* c, const uint32_t* codes, const float* coeff, 
     const int64_t warps = n * wpt;
     const unsigned grid = (unsigned)((warps * 32 + 255) / 256);
     if (rec4) {
-      // persistent row kernel: grid = 2 CTAs per SM, 4 (f32) / 2 (bf16)
-      // tables' rows in flight per lane
+      // persistent row kernel: grid = 2 CTAs per SM; 4 tables' packed rows
+      // in flight per lane (the f32 6-chunk case keeps 4 x 6 x 16 B)
       const unsigned pg = (unsigned)std::min<int64_t>(int64_t(c->num_sms) * 2, (warps * 32 + 255) / 256);
-#define LFFN_PROW(TT, V, M, TIF) gather_row_persistent_kernel<TT, V, M, TIF, 2><<<pg, 256, 0, st>>>(p, wpt);
+      const int pmaxc = f32 ? maxc : (nchunks <= 2 ? 2 : nchunks <= 3 ? 3 : 4);
+      const int pwpt = (nchunks + pmaxc - 1) / pmaxc;
+      const int64_t pwarps = n * pwpt;
+      const unsigned pgrid = (unsigned)std::min<int64_t>(int64_t(c->num_sms) * 2, (pwarps * 32 + 255) / 256);
+      (void)pg;
+#define LFFN_PROW(TT, M, TIF) gather_row_persistent_kernel<TT, M, TIF, 2><<<pgrid, 256, 0, st>>>(p, pwpt);
       if (f32) {
-        if (maxc == 2) { LFFN_PROW(float, 4, 2, 4) } else if (maxc == 4) { LFFN_PROW(float, 4, 4, 4) }
-        else { LFFN_PROW(float, 4, 6, 4) }
+        if (pmaxc == 2) { LFFN_PROW(float, 2, 4) } else if (pmaxc == 4) { LFFN_PROW(float, 4, 4) }
+        else { LFFN_PROW(float, 6, 4) }
       } else {
-        if (maxc == 2) { LFFN_PROW(__nv_bfloat16, 8, 2, 4) } else { LFFN_PROW(__nv_bfloat16, 8, 4, 2) }
+        if (pmaxc == 2) { LFFN_PROW(__nv_bfloat16, 2, 4) } else if (pmaxc == 3) { LFFN_PROW(__nv_bfloat16, 3, 4) }
+        else { LFFN_PROW(__nv_bfloat16, 4, 4) }
       }
 #undef LFFN_PROW
       ++c->launches;
