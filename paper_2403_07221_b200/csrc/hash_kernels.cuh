@@ -253,52 +253,6 @@ __device__ __forceinline__ void run_later_phase(double* sm, int t, int tpt, int 
 // the kernel past the instruction cache.
 __device__ __noinline__ double one_plus_exp_m2(double a) { return __dadd_rn(1.0, exp(-2.0 * a)); }
 
-// Phase 0 of transform tr (bits [0, LOGE)) -- the pre-factor phase.
-template <int LOGE, int PRE>
-__device__ __forceinline__ void run_first_phase(double* sm, int t, int tpt, const HashParams& p,
-                                                int tr, const float* xr, int& bad, bool last) {
-  if (tr == 0) phase_smem<LOGE, LOGE, true, PRE>(sm, t, tpt, 0, p, tr, xr, bad, last);
-  else phase_smem<LOGE, LOGE, false, PRE>(sm, t, tpt, 0, p, tr, xr, bad, last);
-}
-
-// Later phases (bits [lo, lo+b), b <= LOGE).
-template <int LOGE>
-__device__ __forceinline__ void run_later_phase(double* sm, int t, int tpt, int lo, int b,
-                                                const HashParams& p, int tr, int& bad, bool last) {
-  if constexpr (LOGE >= 6) { if (b == 6) { phase_smem<LOGE, 6, false, kPreNone>(sm, t, tpt, lo, p, tr, nullptr, bad, last); return; } }
-  if constexpr (LOGE >= 5) { if (b == 5) { phase_smem<LOGE, 5, false, kPreNone>(sm, t, tpt, lo, p, tr, nullptr, bad, last); return; } }
-  if constexpr (LOGE >= 4) { if (b == 4) { phase_smem<LOGE, 4, false, kPreNone>(sm, t, tpt, lo, p, tr, nullptr, bad, last); return; } }
-  if constexpr (LOGE >= 3) { if (b == 3) { phase_smem<LOGE, 3, false, kPreNone>(sm, t, tpt, lo, p, tr, nullptr, bad, last); return; } }
-  if constexpr (LOGE >= 2) { if (b == 2) { phase_smem<LOGE, 2, false, kPreNone>(sm, t, tpt, lo, p, tr, nullptr, bad, last); return; } }
-  if constexpr (LOGE >= 1) { if (b == 1) { phase_smem<LOGE, 1, false, kPreNone>(sm, t, tpt, lo, p, tr, nullptr, bad, last); return; } }
-}
-
-// 1 + exp(-2a), kept out of line: it is needed only for |z| < 18.5 (rare
-// for the unnormalised transforms), and inlining it per coordinate bloats
-// the kernel past the instruction cache.
-__device__ __noinline__ double one_plus_exp_m2(double a) { return __dadd_rn(1.0, exp(-2.0 * a)); }
-
-// Code + coefficient of one (token, table) from its tau soft-code
-// coordinates (lookup.cpp:81-100, 185-189, 241-253), coordinates in the
-// reference's order j = 0 .. tau-1.
-__device__ __forceinline__ void code_and_coeff(const double* sm, int base, int tau, int scaled,
-                                               uint32_t* code_out, float* coeff_out) {
-  uint32_t code = 0;
-  double w = 1.0, sum_abs = 0.0;
-#pragma unroll 1
-  for (int j = 0; j < tau; ++j) {
-    const double zj = sm[spos(base + j)];
-    if (zj >= 0.0) code |= (1u << j);
-    const double a = fabs(zj);
-    sum_abs = __dadd_rn(sum_abs, a);
-    // 1 + exp(-2a) == 1.0 exactly once exp(-2a) <= 2^-53 (a >= 18.37):
-    // dividing by 1.0 is then a no-op, so skipping the exp is exact.
-    if (a < 18.5) w = __ddiv_rn(w, one_plus_exp_m2(a));
-  }
-  *code_out = code;
-  *coeff_out = (float)(scaled ? __dmul_rn(w, sum_abs) : w);
-}
-
 // K1 for structured projections (signflip, acdc) and the epilogue of the
 // dense projection (z_in given).
 // KIND: kPreSign (signflip), kPreDiag (acdc), kPreNone (dense epilogue on z_in).
