@@ -1,0 +1,122 @@
+// lffn_gpu_dropin.hpp -- reference-side C++ drop-in over the lffn C-ABI.
+//
+// A maintainer of the reference library (lookupffn, namespace lffn) adds this
+// header to their tree and links liblffn_gpu.so.  It restates the
+// reference's public forward entry points with the same signatures, argument
+// meaning and exception types, and runs them on a B200:
+//
+//   lffn::gpu::lookup_forward(x, proj, tables, cfg)   ~ lffn::lookup_forward
+//                                                       (lookup.hpp:124-125)
+//   lffn::gpu::Layer                                   a device-resident layer
+//                                                       for repeated calls
+//
+// It includes the reference's own headers (lookupffn/lookup.hpp,
+// projection.hpp, matrix.hpp, common.hpp) for DenseMatrix / Projection /
+// HashTables / LookupConfig and the error types; nothing here depends on the
+// reference's implementation files.  There is no CPU fallback: a missing
+// device surfaces as std::runtime_error, a LookupCache (training) or
+// neighbor_count > 1 as UsageError.
+#pragma once
+
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "lffn_gpu.h"
+#include "lookupffn/common.hpp"
+#include "lookupffn/lookup.hpp"
+#include "lookupffn/matrix.hpp"
+#include "lookupffn/projection.hpp"
+
+namespace lffn {
+namespace gpu {
+
+inline void check(int status) {
+  if (status == LFFN_OK) return;
+  const std::string msg = lffn_last_error();
+  if (status == LFFN_ERR_USAGE) throw SizeError(msg);
+  if (status == LFFN_ERR_NUMERIC) throw NumericError(msg);
+  throw std::runtime_error("lffn_gpu: " + msg);
+}
+
+inline lffn_cfg to_c(const LookupConfig& c) {
+  lffn_cfg o{};
+  o.d_in = int64_t(c.d_in);
+  o.d_out = int64_t(c.d_out);
+  o.tables = int64_t(c.tables);
+  o.code_bits = int64_t(c.code_bits);
+  o.variant = int32_t(c.variant);
+  o.neighbor_count = int32_t(c.neighbor_count);
+  return o;
+}
+
+inline lffn_proj to_c(const Projection& p) {
+  lffn_proj o{};
+  const ProjectionSpec& s = p.spec();
+  o.kind = int32_t(s.kind);
+  o.d_in = int64_t(s.d_in);
+  o.d_out = int64_t(s.d_out);
+  o.stages = int64_t(s.stages);
+  o.block = int64_t(s.block);
+  o.depth = int64_t(s.depth);
+  o.blob = p.blob().data();
+  o.blob_len = int64_t(p.blob_size());
+  return o;
+}
+
+/// A device-resident LookupFFN layer (one lffn_ctx): tables uploaded once,
+/// then forward() per batch with host DenseMatrix in/out.
+class Layer {
+ public:
+  Layer(const Projection& proj, const HashTables& tables, const LookupConfig& cfg,
+        std::size_t max_tokens, int device = 0, bool bf16_tables = false)
+      : cfg_(cfg) {
+    if (cfg.neighbor_count != 1)
+      throw UsageError("lffn::gpu: the device path implements the top-1 default");
+    const lffn_cfg c = to_c(cfg);
+    const lffn_proj p = to_c(proj);
+    lffn_ctx* ctx = nullptr;
+    check(lffn_ctx_create(&ctx, device, int64_t(max_tokens), &c, &p));
+    ctx_.reset(ctx);
+    if (tables.tables != cfg.tables || tables.code_bits != cfg.code_bits ||
+        tables.d_out != cfg.d_out)
+      throw SizeError("lookup forward: table stack shape mismatch");
+    check(lffn_tables_upload(ctx, tables.data.data(), LFFN_F64,
+                             bf16_tables ? LFFN_BF16 : LFFN_F32));
+  }
+
+  /// y = lookup_forward(x): x rows are rounded to float32 on the way in (the
+  /// reference's own inference path, bench.cpp:115-217, is float32 too).
+  DenseMatrix forward(const DenseMatrix& x) const {
+    if (x.cols != cfg_.d_in) throw SizeError("lookup forward: input width mismatch");
+    std::vector<float> xf(x.data.begin(), x.data.end());
+    std::vector<float> yf(x.rows * cfg_.d_out);
+    check(lffn_forward_host(ctx_.get(), xf.data(), int64_t(x.rows), yf.data()));
+    DenseMatrix y(x.rows, cfg_.d_out);
+    for (std::size_t i = 0; i < yf.size(); ++i) y.data[i] = double(yf[i]);
+    return y;
+  }
+
+ private:
+  struct Deleter {
+    void operator()(lffn_ctx* c) const { lffn_ctx_destroy(c); }
+  };
+  LookupConfig cfg_;
+  std::unique_ptr<lffn_ctx, Deleter> ctx_;
+};
+
+/// Drop-in for lffn::lookup_forward (lookup.hpp:124-125), top-1 only.
+inline DenseMatrix lookup_forward(const DenseMatrix& x, const Projection& proj,
+                                  const HashTables& tables, const LookupConfig& cfg,
+                                  LookupCache* cache = nullptr) {
+  if (cache) throw UsageError("lffn::gpu: LookupCache (training) is not supported on the device");
+  cfg.validate();
+  if (x.cols != cfg.d_in) throw SizeError("lookup forward: input width mismatch");
+  if (proj.spec().d_in != cfg.d_in || proj.spec().d_out != cfg.code_width())
+    throw SizeError("lookup forward: projection must map d_in to h*tau");
+  return Layer(proj, tables, cfg, x.rows > 0 ? x.rows : 1).forward(x);
+}
+
+}  // namespace gpu
+}  // namespace lffn

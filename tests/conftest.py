@@ -27,6 +27,9 @@ def _ensure_built():
     if not os.path.exists(lib):
         subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "paper_2403_07221_b200", "csrc")],
                        check=True)
+    dropin = os.path.join(ROOT, "oracle", "_ref", "dropin_test")
+    if not os.path.exists(dropin) and os.path.isdir("/root/reference/proj/src"):
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "dropin"], check=True)
 
 
 _ensure_built()

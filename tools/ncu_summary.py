@@ -46,7 +46,7 @@ def launches(path):
             continue
         v = float(r[vi].replace(",", ""))
         unit = r[ui]
-        us = v / 1000.0 if unit == "nsecond" else v * (1000.0 if unit == "msecond" else 1.0)
+        us = v / 1000.0 if unit in ("ns", "nsecond") else v * (1000.0 if unit in ("ms", "msecond") else 1.0)
         name = r[ki].split("(")[0]
         a = agg.setdefault(name, [0, 0.0])
         a[0] += 1
@@ -54,10 +54,14 @@ def launches(path):
     total = sum(v[1] for v in agg.values())
     print("| kernel | launches | total us | avg us | share |")
     print("|---|---:|---:|---:|---:|")
+    step = {n: v for n, v in agg.items() if "lffn_gpu::" in n and "l2_read" not in n}
+    stotal = sum(v[1] for v in step.values()) or 1.0
     for name, (cnt, us) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
-        print(f"| `{name}` | {cnt} | {us:.1f} | {us / cnt:.1f} | {100 * us / total:.1f}% |")
-    print(f"\nTotal device time of listed launches: {total:.1f} us "
-          "(cold-cache, serialised under ncu: compare shares, not absolutes).")
+        share = f"{100 * us / stotal:.1f}%" if name in step else "not in step"
+        print(f"| `{name}` | {cnt} | {us:.1f} | {us / cnt:.1f} | {share} |")
+    print(f"\nShare = fraction of the forward's own kernels (hash + gather); the bandwidth "
+          "probe and torch's L2-flush fill run outside the timed step.  Times are cold-cache "
+          "and serialised under ncu: compare shares, not absolutes.")
 
 
 def raw(path):
@@ -102,12 +106,12 @@ def traffic(path, key):
     ki = hdr.index("Kernel Name")
     for row in rows:
         if "gather" in row[ki]:
-            rd = float(row[hdr.index("dram__bytes_read.sum")].replace(",", ""))
-            wr = float(row[hdr.index("dram__bytes_write.sum")].replace(",", ""))
-            ur = units[hdr.index("dram__bytes_read.sum")]
-            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(ur, 1)
-            print(json.dumps({key: {"dram_bytes_per_launch": (rd + wr) * scale,
-                                    "source": path}}))
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            tot = 0.0
+            for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                i = hdr.index(m)
+                tot += float(row[i].replace(",", "")) * scale.get(units[i], 1)
+            print(json.dumps({key: {"dram_bytes_per_launch": tot, "source": path}}))
             return
 
 
