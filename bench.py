@@ -77,18 +77,56 @@ def cpu_model() -> str:
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled DURING the timed region: NVML
+    polled every 2 ms from a thread (the timed region is tens of ms), falling
+    back to `nvidia-smi -lms` when NVML is unavailable."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NVML_REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+                    0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, device: int):
         self.device = device
         self.proc = None
         self.lines = []
+        self.nvml = None
+        self.stop = threading.Event()
+
+    def _poll_nvml(self):
+        import pynvml as N
+
+        while not self.stop.is_set():
+            try:
+                sm = N.nvmlDeviceGetClockInfo(self.nvml, N.NVML_CLOCK_SM)
+                mx = N.nvmlDeviceGetMaxClockInfo(self.nvml, N.NVML_CLOCK_SM)
+                rs = N.nvmlDeviceGetCurrentClocksEventReasons(self.nvml)
+                names = [nm for bit, nm in self.NVML_REASONS.items() if rs & bit]
+                self.lines.append((float(sm), float(mx), names))
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def __enter__(self):
+        try:
+            import pynvml as N
+
+            N.nvmlInit()
+            import torch
+
+            # map the CUDA ordinal to the NVML handle through the PCI address
+            pr = torch.cuda.get_device_properties(self.device)
+            try:
+                bus = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+                self.nvml = N.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                self.nvml = N.nvmlDeviceGetHandleByIndex(self.device)
+            self.t = threading.Thread(target=self._poll_nvml, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
@@ -109,6 +147,9 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        self.stop.set()
+        if self.nvml is not None:
+            self.t.join(timeout=1)
         if self.proc:
             self.proc.terminate()
             try:
@@ -117,6 +158,14 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
+        if self.nvml is not None:
+            if not self.lines:
+                return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+            sm = [s for s, _, _ in self.lines]
+            reasons = sorted({r for _, _, rs in self.lines for r in rs})
+            return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(m for _, m, _ in self.lines),
+                    "sm_mhz_min": min(sm), "reasons": reasons, "samples": len(sm),
+                    "source": "nvml"}
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:

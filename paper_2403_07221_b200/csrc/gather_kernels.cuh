@@ -30,6 +30,7 @@ struct GatherParams {
   int d_out;
   int accumulate;
   int* flag;
+  int reverse_odd_rounds;   // persistent kernel: odd rounds walk the tables backwards
 };
 
 template <typename TT, int VEC>
@@ -303,14 +304,20 @@ __global__ void __launch_bounds__(256, MINB) gather_row_persistent_kernel(Gather
     for (int c = 0; c < MAXC; ++c)
 #pragma unroll
       for (int v = 0; v < VEC; ++v) acc[c][v] = 0.f;
-    uint4 cc = __ldg(reinterpret_cast<const uint4*>(cr));
-    float4 ww = __ldg(reinterpret_cast<const float4*>(wr));
-    for (int kg = 0; kg < p.nk; kg += 4) {
+    // Optionally every other round of tokens walks the tables backwards, so
+    // the tables a round finishes with (still in L2) are the first the next
+    // round reads.
+    const int rmask = (p.reverse_odd_rounds && ((item / nwarps) & 1)) ? -1 : 0;
+    auto group_of = [&](int it) { return rmask ? p.nk - 4 - it : it; };
+    uint4 cc = __ldg(reinterpret_cast<const uint4*>(cr + group_of(0)));
+    float4 ww = __ldg(reinterpret_cast<const float4*>(wr + group_of(0)));
+    for (int it = 0; it < p.nk; it += 4) {
+      const int kg = group_of(it);
       uint4 cn = cc;
       float4 wn = ww;
-      if (kg + 4 < p.nk) {
-        cn = __ldg(reinterpret_cast<const uint4*>(cr + kg + 4));
-        wn = __ldg(reinterpret_cast<const float4*>(wr + kg + 4));
+      if (it + 4 < p.nk) {
+        cn = __ldg(reinterpret_cast<const uint4*>(cr + group_of(it + 4)));
+        wn = __ldg(reinterpret_cast<const float4*>(wr + group_of(it + 4)));
       }
       const uint32_t codes4[4] = {cc.x, cc.y, cc.z, cc.w};
       const float w4[4] = {ww.x, ww.y, ww.z, ww.w};

@@ -14,6 +14,7 @@
 
 #include "gather_kernels.cuh"
 #include "hash_kernels.cuh"
+#include "hash_pair_kernel.cuh"
 #include "lffn_gpu.h"
 #include "lffn_internal.h"
 #include "staged_gather.cuh"
@@ -200,6 +201,29 @@ int launch_hash(lffn_ctx* c, const float* d_x, int64_t n, uint32_t* codes, float
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     kernel<<<grid, block, smem, st>>>(p);
   };
+  // the pair kernel is exact but measured slower (shuffle traffic throttles
+  // the MIO queue: c2 hash 0.46 vs 0.23 ms), so it is opt-in
+  static const int use_pair = getenv("LFFN_HASH_PAIR") ? atoi(getenv("LFFN_HASH_PAIR")) : 0;
+  if (use_pair && (c->logD == 11 || c->logD == 12) && kind != kPreNone) {
+    // D = 2048 / 4096: the 32-element pair kernel (hash_pair_kernel.cuh)
+    const int tpb2 = c->logD == 11 ? 2 : 1;
+    const size_t smem2 = size_t(tpb2) * size_t(pair_padded_len(int(c->D))) * sizeof(double);
+    const unsigned grid2 = (unsigned)((n + tpb2 - 1) / tpb2);
+    auto go2 = [&](auto kernel) {
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2));
+      kernel<<<grid2, 128, smem2, st>>>(p);
+    };
+    if (c->logD == 11) {
+      if (kind == kPreSign) go2(hash_pair_kernel<11, kPreSign>);
+      else go2(hash_pair_kernel<11, kPreDiag>);
+    } else {
+      if (kind == kPreSign) go2(hash_pair_kernel<12, kPreSign>);
+      else go2(hash_pair_kernel<12, kPreDiag>);
+    }
+    ++c->launches;
+    LFFN_CUDA(cudaGetLastError());
+    return LFFN_OK;
+  }
   if (nt == 128 && kind == kPreSign) {  // tuning variants (LFFN_HASH_VARIANT)
     if (hvar == 1) go(hash_structured_kernel<6, kPreSign, 128, 3>);
     else if (hvar == 2) go(hash_structured_kernel<6, kPreSign, 128, 2>);
@@ -245,6 +269,8 @@ int launch_gather_group(lffn_ctx* c, const uint32_t* codes, const float* coeff, 
   p.d_out = int(c->cfg.d_out);
   p.accumulate = accumulate;
   p.flag = c->d_flag;
+  static const int rev = getenv("LFFN_GATHER_REVERSE") ? atoi(getenv("LFFN_GATHER_REVERSE")) : 0;
+  p.reverse_odd_rounds = rev;
   if (staged_gather_applicable(c->staged_ok, p, c->t_dtype)) {
     int rc = launch_staged_gather(p, c->t_dtype, c->staged_smem, st);
     ++c->launches;
