@@ -138,6 +138,24 @@ int lffn_tables_upload(lffn_ctx* ctx, const void* host_T, int host_dtype, int st
  * [table_end-table_begin][2^tau][d_out] in dtype (no copy). */
 int lffn_tables_attach(lffn_ctx* ctx, const void* d_T, int dtype);
 
+/* ---- checkpoints: the reference's "LFFN" v1 file (checkpoint.hpp:17-26) --
+ * header -> cfg (neighbor_count 1) + projection spec (proj->blob NULL,
+ * proj->blob_len set) + total table length; load -> float64 blob and tables;
+ * save writes the same format (save_checkpoint, checkpoint.cpp:52-84).
+ * Errors: status 1 with the reference's messages (bad magic, unsupported
+ * version, bad variant/kind byte, truncated file, trailing bytes). */
+int lffn_checkpoint_header(const char* path, lffn_cfg* cfg, lffn_proj* proj, int64_t* tables_len);
+int lffn_checkpoint_load(const char* path, double* blob, double* tables);
+int lffn_checkpoint_save(const char* path, const lffn_cfg* cfg, const lffn_proj* proj,
+                         const double* tables);
+/* Context straight from a checkpoint (load_checkpoint, checkpoint.cpp:86-138):
+ * tables [table_begin, table_end) (0, 0 = all) are streamed from the file
+ * into the device copy in store_dtype without materialising the whole stack
+ * on the host. */
+int lffn_ctx_create_from_checkpoint(lffn_ctx** out, int device, int64_t max_tokens,
+                                    const char* path, int store_dtype, int64_t table_begin,
+                                    int64_t table_end);
+
 /* Hash stage = Projection::forward (projection.cpp:167-266) + compute_codes
  * (lookup.cpp:81-100) + top-1 weight (lookup.cpp:185-189), i.e. the
  * lookup_hash_f32 + lookup_weights_f32 pair (bench.cpp:115-180), in one

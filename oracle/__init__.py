@@ -282,6 +282,9 @@ class Reference:
                                          [C.c_int64] * 3 + [_f64, C.c_int64, _f64, _f64,
                                                             C.c_size_t, _f64] + [C.c_void_p] * 4)
         L.ref_lookup_flops.argtypes = [C.c_int64] * 5 + [C.c_int] + [C.c_int64] * 3 + [_f64]
+        L.ref_save_checkpoint.argtypes = ([C.c_char_p] + [C.c_int64] * 4 + [C.c_int, C.c_int] +
+                                          [C.c_int64] * 3 + [_f64, C.c_int64, _f64])
+        L.ref_load_checkpoint.argtypes = [C.c_char_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.ref_pipeline_f32.argtypes = ([C.c_int64] * 4 + [C.c_int, C.c_int] + [C.c_int64] * 3 +
                                        [_f32, _f32, _f32, C.c_size_t, _f32, C.c_int, C.c_int,
                                         C.c_int])
@@ -388,6 +391,34 @@ class Reference:
         if want_cache:
             return y, dict(z=z, codes=codes, weights=w, dots=dots)
         return y
+
+    def save_checkpoint(self, path: str, c: Cfg, s: Spec, blob, tables) -> None:
+        blob = np.ascontiguousarray(blob, np.float64)
+        rc = self.lib.ref_save_checkpoint(os.fsencode(path), c.d_in, c.d_out, c.tables,
+                                          c.code_bits, c.variant, s.kind, s.stages, s.block,
+                                          s.depth, blob, blob.size,
+                                          np.ascontiguousarray(tables, np.float64))
+        if rc:
+            self._err(rc)
+
+    def load_checkpoint(self, path: str):
+        """-> (header dict, blob, tables) through the reference's load_checkpoint."""
+        hdr = np.zeros(8, np.int64)
+        rc = self.lib.ref_load_checkpoint(os.fsencode(path), hdr.ctypes.data, None, None)
+        if rc:
+            self._err(rc)
+        keys = ["d_in", "d_out", "tables", "code_bits", "variant", "kind", "m", "b"]
+        h = dict(zip(keys, hdr.tolist()))
+        c = Cfg(h["d_in"], h["d_out"], h["tables"], h["code_bits"], h["variant"])
+        s = c.spec(h["kind"], stages=h["m"] if h["kind"] == BH else 4, block=h["b"],
+                   depth=h["m"] if h["kind"] == ACDC else 1)
+        blob = np.empty(s.blob_size(), np.float64)
+        T = np.empty(c.tables * c.rows * c.d_out, np.float64)
+        rc = self.lib.ref_load_checkpoint(os.fsencode(path), hdr.ctypes.data, blob.ctypes.data,
+                                          T.ctypes.data)
+        if rc:
+            self._err(rc)
+        return h, blob, T
 
     def lookup_flops(self, c: Cfg, s: Spec):
         out = np.zeros(3, np.float64)

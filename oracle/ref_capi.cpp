@@ -16,6 +16,7 @@
 #include <exception>
 #include <vector>
 
+#include "lookupffn/checkpoint.hpp"
 #include "lookupffn/common.hpp"
 #include "lookupffn/flops.hpp"
 #include "lookupffn/fwht.hpp"
@@ -192,6 +193,46 @@ int ref_lookup_forward(int64_t d_in, int64_t d_out, int64_t h, int64_t tau, int 
     if (weights_out)
       std::memcpy(weights_out, cache.weights.data(), cache.weights.size() * sizeof(double));
     if (dots_out) std::memcpy(dots_out, cache.dots.data(), cache.dots.size() * sizeof(double));
+    return 0;
+  } catch (const std::exception& e) {
+    return map_exc(e);
+  }
+}
+
+// save_checkpoint / load_checkpoint (checkpoint.cpp:52-138).  load returns
+// the header fields in hdr[8] = {d_in, d_out, h, tau, variant, kind, m, b}
+// and copies blob / tables when the pointers are non-null.
+int ref_save_checkpoint(const char* path, int64_t d_in, int64_t d_out, int64_t h, int64_t tau,
+                        int variant, int kind, int64_t stages, int64_t block, int64_t depth,
+                        const double* blob, int64_t blob_len, const double* tables) {
+  try {
+    CheckpointModel m;
+    m.cfg = make_cfg(d_in, d_out, h, tau, variant, 1);
+    m.proj = Projection::from_blob(make_spec(kind, d_in, h * tau, stages, block, depth),
+                                   std::vector<double>(blob, blob + blob_len));
+    m.tables = HashTables::zeros_like(m.cfg);
+    std::memcpy(m.tables.data.data(), tables, m.tables.data.size() * sizeof(double));
+    save_checkpoint(path, m);
+    return 0;
+  } catch (const std::exception& e) {
+    return map_exc(e);
+  }
+}
+
+int ref_load_checkpoint(const char* path, int64_t* hdr, double* blob, double* tables) {
+  try {
+    CheckpointModel m = load_checkpoint(path);
+    const ProjectionSpec& s = m.proj.spec();
+    hdr[0] = int64_t(m.cfg.d_in);
+    hdr[1] = int64_t(m.cfg.d_out);
+    hdr[2] = int64_t(m.cfg.tables);
+    hdr[3] = int64_t(m.cfg.code_bits);
+    hdr[4] = int64_t(m.cfg.variant);
+    hdr[5] = int64_t(s.kind);
+    hdr[6] = int64_t(s.kind == ProjKind::acdc ? s.depth : s.stages);
+    hdr[7] = int64_t(s.block);
+    if (blob) std::memcpy(blob, m.proj.blob().data(), m.proj.blob_size() * sizeof(double));
+    if (tables) std::memcpy(tables, m.tables.data.data(), m.tables.data.size() * sizeof(double));
     return 0;
   } catch (const std::exception& e) {
     return map_exc(e);

@@ -17,15 +17,18 @@ from .lookup import (
     Projection,
     ProjectionSpec,
     ProjKind,
+    checkpoint_header,
     fill_gaussian,
     fill_signs,
     gaussian_matrix,
+    load_checkpoint,
     lookup_forward,
+    save_checkpoint,
     to_bf16_values,
 )
 
 __all__ = [
     "HashTables", "LookupConfig", "LookupFFN", "LookupVariant", "Projection", "ProjectionSpec",
     "ProjKind", "fill_gaussian", "fill_signs", "gaussian_matrix", "lookup_forward",
-    "to_bf16_values", "flops", "LffnError", "NumericError", "SizeError", "UsageError",
+    "to_bf16_values", "flops", "checkpoint_header", "load_checkpoint", "save_checkpoint", "LffnError", "NumericError", "SizeError", "UsageError",
 ]

@@ -43,6 +43,12 @@ SIGNATURES = {
     "lffn_fill_signs": (C.c_int, [C.c_uint64, _VP, _I64]),
     "lffn_tables_init": (C.c_int, [C.POINTER(lffn_cfg), C.c_uint64, _VP]),
     "lffn_convert": (C.c_int, [_VP, C.c_int, _VP, C.c_int, _I64]),
+    "lffn_checkpoint_header": (C.c_int, [C.c_char_p, C.POINTER(lffn_cfg), C.POINTER(lffn_proj),
+                                         C.POINTER(_I64)]),
+    "lffn_checkpoint_load": (C.c_int, [C.c_char_p, _VP, _VP]),
+    "lffn_checkpoint_save": (C.c_int, [C.c_char_p, C.POINTER(lffn_cfg), C.POINTER(lffn_proj), _VP]),
+    "lffn_ctx_create_from_checkpoint": (C.c_int, [C.POINTER(_VP), C.c_int, _I64, C.c_char_p,
+                                                  C.c_int, _I64, _I64]),
     "lffn_ctx_create": (C.c_int, [C.POINTER(_VP), C.c_int, _I64, C.POINTER(lffn_cfg),
                                   C.POINTER(lffn_proj)]),
     "lffn_ctx_create_shard": (C.c_int, [C.POINTER(_VP), C.c_int, _I64, C.POINTER(lffn_cfg),

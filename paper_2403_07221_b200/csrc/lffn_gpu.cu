@@ -424,6 +424,55 @@ float bf16_to_f32(uint16_t b) {
 
 }  // namespace
 
+namespace lffn_gpu {
+
+// Converts host tables [k0, k0+nk) of the context's slice (host points at
+// table k0) to store_dtype and copies them to the device; (re)allocates the
+// device slice when needed.
+int tables_upload_range(lffn_ctx* c, const void* host, int host_dtype, int store_dtype, int64_t k0,
+                        int64_t nk) {
+  if (store_dtype != LFFN_F32 && store_dtype != LFFN_BF16)
+    return fail(LFFN_ERR_USAGE, "tables upload: store dtype must be f32 or bf16");
+  if (host_dtype < LFFN_F32 || host_dtype > LFFN_F64)
+    return fail(LFFN_ERR_USAGE, "tables upload: unknown host dtype");
+  if (k0 < 0 || nk < 0 || k0 + nk > c->h_loc)
+    return fail(LFFN_ERR_USAGE, "tables upload: table range outside the context's slice");
+  DeviceGuard g(c->device);
+  const size_t per_table = size_t(c->rows) * size_t(c->cfg.d_out);
+  const size_t esz = store_dtype == LFFN_F32 ? 4 : 2;
+  if (!c->d_T_owned || c->t_dtype != store_dtype || c->d_T != c->d_T_owned) {
+    if (c->d_T_owned) cudaFree(c->d_T_owned);
+    c->d_T_owned = nullptr;
+    void* d = nullptr;
+    LFFN_CUDA(cudaMalloc(&d, std::max<size_t>(per_table * size_t(c->h_loc) * esz, 16)));
+    c->d_T_owned = d;
+    c->d_T = d;
+    c->t_dtype = store_dtype;
+  }
+  const size_t count = per_table * size_t(nk);
+  std::vector<unsigned char> staging(count * esz);
+  for (size_t i = 0; i < count; ++i) {
+    if (store_dtype == LFFN_F32) {
+      float f;
+      if (host_dtype == LFFN_F64) f = float(static_cast<const double*>(host)[i]);
+      else if (host_dtype == LFFN_F32) f = static_cast<const float*>(host)[i];
+      else f = bf16_to_f32(static_cast<const uint16_t*>(host)[i]);
+      std::memcpy(&staging[i * 4], &f, 4);
+    } else {
+      const uint16_t b = host_dtype == LFFN_BF16 ? static_cast<const uint16_t*>(host)[i]
+                         : host_dtype == LFFN_F64
+                             ? f64_to_bf16_rne(static_cast<const double*>(host)[i])
+                             : f32_to_bf16_rne(static_cast<const float*>(host)[i]);
+      std::memcpy(&staging[i * 2], &b, 2);
+    }
+  }
+  LFFN_CUDA(cudaMemcpy(static_cast<char*>(c->d_T_owned) + size_t(k0) * per_table * esz,
+                       staging.data(), staging.size(), cudaMemcpyHostToDevice));
+  return LFFN_OK;
+}
+
+}  // namespace lffn_gpu
+
 extern "C" {
 
 const char* lffn_last_error(void) { return g_last_error.c_str(); }
@@ -560,42 +609,17 @@ int64_t lffn_ctx_launch_count(const lffn_ctx* ctx) { return ctx ? ctx->launches 
 
 int lffn_tables_upload(lffn_ctx* c, const void* host_T, int host_dtype, int store_dtype) {
   if (!c || !host_T) return fail(LFFN_ERR_USAGE, "tables upload: null argument");
-  if (store_dtype != LFFN_F32 && store_dtype != LFFN_BF16)
-    return fail(LFFN_ERR_USAGE, "tables upload: store dtype must be f32 or bf16");
-  if (host_dtype < LFFN_F32 || host_dtype > LFFN_F64)
-    return fail(LFFN_ERR_USAGE, "tables upload: unknown host dtype");
-  DeviceGuard g(c->device);
   const size_t per_table = size_t(c->rows) * size_t(c->cfg.d_out);
-  const size_t count = per_table * size_t(c->h_loc);
-  const size_t first = per_table * size_t(c->kb);
-  const size_t esz = store_dtype == LFFN_F32 ? 4 : 2;
-  std::vector<unsigned char> staging(count * esz);
-  for (size_t i = 0; i < count; ++i) {
-    float f;
-    if (host_dtype == LFFN_F64) f = float(static_cast<const double*>(host_T)[first + i]);
-    else if (host_dtype == LFFN_F32) f = static_cast<const float*>(host_T)[first + i];
-    else f = bf16_to_f32(static_cast<const uint16_t*>(host_T)[first + i]);
-    if (store_dtype == LFFN_F32) {
-      std::memcpy(&staging[i * 4], &f, 4);
-    } else {
-      const uint16_t b = host_dtype == LFFN_BF16
-                             ? static_cast<const uint16_t*>(host_T)[first + i]
-                             : host_dtype == LFFN_F64
-                                   ? f64_to_bf16_rne(static_cast<const double*>(host_T)[first + i])
-                                   : f32_to_bf16_rne(f);
-      std::memcpy(&staging[i * 2], &b, 2);
-    }
+  const size_t hsz = host_dtype == LFFN_F64 ? 8 : host_dtype == LFFN_F32 ? 4 : 2;
+  const char* first = static_cast<const char*>(host_T) + size_t(c->kb) * per_table * hsz;
+  // bounded staging: convert and copy ~64 MB of host tables at a time
+  const int64_t chunk = std::max<int64_t>(1, int64_t((size_t(64) << 20) / (per_table * hsz)));
+  for (int64_t k0 = 0; k0 < c->h_loc; k0 += chunk) {
+    const int64_t nk = std::min(chunk, c->h_loc - k0);
+    if (int rc = tables_upload_range(c, first + size_t(k0) * per_table * hsz, host_dtype,
+                                     store_dtype, k0, nk))
+      return rc;
   }
-  if (c->d_T_owned) {
-    cudaFree(c->d_T_owned);
-    c->d_T_owned = nullptr;
-  }
-  void* d = nullptr;
-  LFFN_CUDA(cudaMalloc(&d, std::max<size_t>(staging.size(), 16)));
-  LFFN_CUDA(cudaMemcpy(d, staging.data(), staging.size(), cudaMemcpyHostToDevice));
-  c->d_T_owned = d;
-  c->d_T = d;
-  c->t_dtype = store_dtype;
   return LFFN_OK;
 }
 

@@ -18,6 +18,11 @@ int64_t blob_size(const lffn_proj* p);
 int validate_cfg(const lffn_cfg* c);
 int validate_proj(const lffn_proj* p);
 
+// Host tables [k0, k0+nk) of a context's slice -> device (checkpoint.cpp
+// streams through this).
+int tables_upload_range(lffn_ctx* c, const void* host, int host_dtype, int store_dtype, int64_t k0,
+                        int64_t nk);
+
 // Device non-finite flag bits; each names the reference stage that would
 // throw NumericError (lookup.cpp:204,269; projection.cpp:172,264).
 enum : int {

@@ -28,6 +28,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import os
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -39,6 +40,7 @@ from ._capi import LFFN_BF16, LFFN_F32, LFFN_F64, NumericError, SizeError, Usage
 __all__ = [
     "LookupVariant", "ProjKind", "LookupConfig", "ProjectionSpec", "Projection", "HashTables",
     "LookupFFN", "lookup_forward", "fill_gaussian", "fill_signs", "gaussian_matrix",
+    "checkpoint_header", "load_checkpoint", "save_checkpoint",
     "to_bf16_values", "SizeError", "UsageError", "NumericError",
 ]
 
@@ -227,6 +229,33 @@ def to_bf16_values(a: np.ndarray) -> np.ndarray:
     return (bits.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
 
 
+def checkpoint_header(path: str):
+    """(LookupConfig, ProjectionSpec, tables_len) of an "LFFN" v1 checkpoint."""
+    c, p, nt = _capi.lffn_cfg(), _capi.lffn_proj(), C.c_int64()
+    check(_capi.lib().lffn_checkpoint_header(os.fsencode(path), C.byref(c), C.byref(p),
+                                             C.byref(nt)))
+    cfg = LookupConfig(c.d_in, c.d_out, c.tables, c.code_bits, LookupVariant(c.variant),
+                       c.neighbor_count)
+    spec = ProjectionSpec(p.d_in, p.d_out, ProjKind(p.kind), p.stages, p.block, p.depth)
+    return cfg, spec, int(nt.value)
+
+
+def load_checkpoint(path: str):
+    """load_checkpoint (checkpoint.cpp:86-138) -> (cfg, Projection, HashTables)."""
+    cfg, spec, nt = checkpoint_header(path)
+    blob = np.empty(spec.blob_size(), np.float64)
+    data = np.empty(nt, np.float64)
+    check(_capi.lib().lffn_checkpoint_load(os.fsencode(path), blob.ctypes.data, data.ctypes.data))
+    return cfg, Projection(spec, blob), HashTables(cfg.tables, cfg.code_bits, cfg.d_out, data)
+
+
+def save_checkpoint(path: str, cfg: LookupConfig, proj: Projection, tables: HashTables) -> None:
+    """save_checkpoint (checkpoint.cpp:52-84): the reference's "LFFN" v1 format."""
+    data = np.ascontiguousarray(tables.data, np.float64)
+    check(_capi.lib().lffn_checkpoint_save(os.fsencode(path), C.byref(cfg._c()),
+                                           C.byref(proj._c()), data.ctypes.data))
+
+
 _DTYPES = {"f32": LFFN_F32, "float32": LFFN_F32, "bf16": LFFN_BF16, "bfloat16": LFFN_BF16}
 
 
@@ -253,6 +282,26 @@ class LookupFFN:
         self.table_range = (kb, ke)
         if tables is not None:
             self.upload_tables(tables)
+
+    @classmethod
+    def from_checkpoint(cls, path: str, *, device: int = 0, max_tokens: int = 65536,
+                        table_dtype: str = "f32",
+                        table_range: Optional[tuple] = None) -> "LookupFFN":
+        """A layer straight from an "LFFN" v1 checkpoint (load_checkpoint,
+        checkpoint.cpp:86-138); the tables stream from the file to the GPU."""
+        cfg, spec, _ = checkpoint_header(path)
+        self = cls.__new__(cls)
+        self.cfg, self.proj, self.device = cfg, spec, device
+        self.max_tokens = max_tokens
+        self.table_dtype = _DTYPES[table_dtype]
+        kb, ke = table_range if table_range is not None else (0, cfg.tables)
+        ctx = C.c_void_p()
+        check(_capi.lib().lffn_ctx_create_from_checkpoint(C.byref(ctx), device, max_tokens,
+                                                          os.fsencode(path), self.table_dtype,
+                                                          kb, ke))
+        self._ctx = ctx
+        self.table_range = (kb, ke)
+        return self
 
     # -- tables ----------------------------------------------------------
     def upload_tables(self, tables) -> None:
