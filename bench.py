@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2")
-    ap.add_argument("--kind", default="signflip", choices=["signflip", "dense", "acdc"])
+    ap.add_argument("--kind", default="signflip", choices=["signflip", "dense", "acdc", "bh"])
     ap.add_argument("--tokens", type=int, default=0, help="override the batch size")
     ap.add_argument("--cpu-sample", type=int, default=0, help="reference-arm tokens per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")

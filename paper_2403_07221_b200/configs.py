@@ -49,6 +49,11 @@ def config_of(w: Workload) -> LookupConfig:
 
 
 def spec_of(w: Workload, kind: ProjKind = ProjKind.signflip) -> ProjectionSpec:
+    """signflip (primary), dense, acdc (depth 2) or the paper's BH4 with b = 64."""
+    if kind == ProjKind.bh:
+        return ProjectionSpec(w.d, w.h * w.tau, kind, stages=4, block=min(64, w.d))
+    if kind == ProjKind.acdc:
+        return ProjectionSpec(w.d, w.h * w.tau, kind, depth=2)
     return ProjectionSpec(w.d, w.h * w.tau, kind)
 
 

@@ -1,0 +1,148 @@
+// hash_bh_kernel.cuh -- K1 for the BH{m} projection (the
+// paper's recommended BH4), fused with codes and coefficients.
+//
+// Reference: Projection::forward bh branch (projection.cpp:217-228): per
+// stage s, dst = block_diag_apply(buf, B_s) (projection.hpp:101-119:
+// dst[g*b+c] = sum_r src[g*b+r] * B_s[g][r][c], r ascending, from 0.0), then
+// fwht_kernel(dst) (fwht.hpp:28-41).
+//
+// Device form: a CTA of 512 threads owns T = 16384 / D tokens whose D-vectors
+// live in shared memory.  The block-diagonal multiply gives every thread 32
+// (token, column) outputs, accumulated in the reference's order with
+// separately rounded multiply and add, so z stays bit-identical to the
+// reference; each B_s element is read once per CTA and used for T tokens.
+// The Hadamard stages then run with the 32-element register phases of
+// hash_structured_kernel, and the epilogue packs codes / coefficients.
+// Float64 arithmetic: 2*D*b + D*log2(D) flops per stage per token
+// (flops.cpp:27-33).
+#pragma once
+
+#include "hash_kernels.cuh"
+
+namespace lffn_gpu {
+
+struct BhParams {
+  const double* blocks;  // m stages x (D/b) blocks x b x b, row-major (projection.hpp:47-54)
+  int b, logb;
+  int stages;
+};
+
+template <int LOGE>
+__global__ void __launch_bounds__(512, 1) hash_bh_kernel(HashParams p, BhParams bh) {
+  extern __shared__ double smem[];
+  constexpr int E = 1 << LOGE;
+  constexpr int NT = 512;
+  constexpr int PAIRS = 32;  // (token, column) outputs per thread per stage
+  const int D = p.D, logD = p.logD;
+  const int pad = padded_len(D);
+  const int T = p.tokens_per_block;  // T * D == NT * PAIRS
+  const int tpt = p.threads_per_token;
+  const int64_t tok0 = (int64_t)blockIdx.x * T;
+  const int tid = threadIdx.x;
+  int bad = 0;
+
+  // pad x to D (projection.cpp:212-213), fp32 -> fp64 exactly
+  for (int q = tid; q < T * D; q += NT) {
+    const int t = q >> logD, a = q & (D - 1);
+    const int64_t token = tok0 + t;
+    double v = 0.0;
+    if (token < p.n && a < p.d_in) {
+      const float f = __ldg(p.x + token * p.d_in + a);
+      if (!isfinite(f)) bad |= 1;
+      v = (double)f;
+    }
+    smem[t * pad + spos(a)] = v;
+  }
+  __syncthreads();
+
+  const int b = bh.b, logb = bh.logb;
+  const size_t stage_size = (size_t)(D >> logb) * b * b;
+  int nph = 1;
+  if constexpr (LOGE > 0) nph = (logD + LOGE - 1) / LOGE;
+  for (int s = 0; s < bh.stages; ++s) {
+    // ---- block-diagonal multiply (projection.hpp:101-119)
+    const double* Bs = bh.blocks + s * stage_size;
+    double acc[PAIRS];
+#pragma unroll
+    for (int j = 0; j < PAIRS; ++j) acc[j] = 0.0;
+    for (int r = 0; r < b; ++r) {
+#pragma unroll
+      for (int j = 0; j < PAIRS; ++j) {
+        const int q = tid + NT * j;
+        const int t = q >> logD, c = q & (D - 1);
+        const int g = c >> logb, cc = c & (b - 1);
+        const double bv = __ldg(Bs + ((size_t)g * b + r) * b + cc);
+        const double sv = smem[t * pad + spos((g << logb) + r)];
+        acc[j] = __dadd_rn(acc[j], __dmul_rn(sv, bv));
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < PAIRS; ++j) {
+      const int q = tid + NT * j;
+      smem[(q >> logD) * pad + spos(q & (D - 1))] = acc[j];
+    }
+    __syncthreads();
+    // ---- Hadamard transform of every token (fwht.hpp:28-41)
+    const bool last_stage = s == bh.stages - 1;
+    for (int ph = 0; ph < nph; ++ph) {
+      const int lo = ph * LOGE;
+      const int bits = min(LOGE, logD - lo);
+      for (int slot = tid / tpt; slot < T; slot += NT / tpt) {
+        double* sm = smem + slot * pad;
+        const int tt = tid % tpt;
+        const bool last = last_stage && ph == nph - 1 && tok0 + slot < p.n;
+        if (ph == 0) {
+          phase_smem<LOGE, LOGE, false, kPreNone>(sm, tt, tpt, 0, p, s, nullptr, bad, last);
+        } else {
+          run_later_phase<LOGE>(sm, tt, tpt, lo, bits, p, s, bad, last);
+        }
+      }
+      __syncthreads();
+    }
+  }
+
+  // ---- codes + coefficients (lookup.cpp:81-100, 185-189), per token slot
+  for (int slot = tid / tpt; slot < T; slot += NT / tpt) {
+    const int64_t token = tok0 + slot;
+    if (token >= p.n) continue;
+    const double* sm = smem + slot * pad;
+    const int t = tid % tpt;
+    if (p.z_out || p.code_width != D) {
+      for (int a = t; a < p.code_width; a += tpt) {
+        const double zv = sm[spos(a)];
+        if (!isfinite(zv)) bad |= 2;
+        if (p.z_out) p.z_out[token * p.code_width + a] = zv;
+      }
+    }
+    const int tau = p.tau;
+    const int hl = p.ke - p.kb;
+    const int a_lo = t * E;
+    const int a_hi = min(a_lo + E, p.code_width);
+    for (int k = max((a_lo + tau - 1) / tau, p.kb); k < p.ke && k * tau < a_hi; ++k) {
+      const int base = k * tau;
+      uint32_t code = 0;
+      bool small = false;
+      double sum_abs = 0.0;
+      for (int j = 0; j < tau; ++j) {
+        const double zj = sm[spos(base + j)];
+        code |= (zj >= 0.0 ? 1u : 0u) << j;
+        const double az = fabs(zj);
+        small |= az < 18.5;
+        sum_abs = __dadd_rn(sum_abs, az);
+      }
+      double w = 1.0;
+      if (small) {
+        for (int j = 0; j < tau; ++j) {
+          const double az = fabs(sm[spos(base + j)]);
+          if (az < 18.5) w = __ddiv_rn(w, one_plus_exp_m2(az));
+        }
+      }
+      p.codes[token * hl + (k - p.kb)] = code;
+      p.coeff[token * hl + (k - p.kb)] = (float)(p.scaled ? __dmul_rn(w, sum_abs) : w);
+    }
+  }
+  if (bad) atomicOr(p.flag, bad);
+}
+
+}  // namespace lffn_gpu

@@ -14,6 +14,7 @@
 
 #include "gather_kernels.cuh"
 #include "hash_kernels.cuh"
+#include "hash_bh_kernel.cuh"
 #include "hash_pair_kernel.cuh"
 #include "lffn_gpu.h"
 #include "lffn_internal.h"
@@ -53,6 +54,7 @@ struct lffn_ctx {
   uint32_t* d_signmask = nullptr;
   double* d_diag = nullptr;
   double* d_W = nullptr;
+  double* d_bh = nullptr;   // bh: m x (D/b) x b x b blocks (float64)
   double* d_zbuf = nullptr;  // dense: [max_tokens x code_width] float64
 
   // tables
@@ -117,6 +119,7 @@ void destroy_ctx(lffn_ctx* c) {
   cudaFree(c->d_signmask);
   cudaFree(c->d_diag);
   cudaFree(c->d_W);
+  cudaFree(c->d_bh);
   cudaFree(c->d_zbuf);
   cudaFree(c->d_T_owned);
   cudaFree(c->d_codes);
@@ -170,6 +173,35 @@ int launch_hash(lffn_ctx* c, const float* d_x, int64_t n, uint32_t* codes, float
   p.codes = codes;
   p.coeff = coeff;
   p.flag = c->d_flag;
+  if (c->proj.kind == LFFN_PROJ_BH) {
+    // BH{m}: fused block-diagonal + Hadamard stages (hash_bh_kernel.cuh)
+    const int loge5 = c->logD >= 5 ? 5 : int(c->logD);
+    const int E5 = 1 << loge5;
+    BhParams bh{};
+    bh.blocks = c->d_bh;
+    bh.b = int(c->proj.block == 0 ? c->D : c->proj.block);
+    bh.logb = ilog2(bh.b);
+    bh.stages = int(c->proj.stages);
+    p.tokens_per_block = int(16384 / c->D);
+    p.threads_per_token = int(c->D / E5);
+    const size_t smem = size_t(p.tokens_per_block) * size_t(padded_len(int(c->D))) * sizeof(double);
+    const unsigned grid = (unsigned)((n + p.tokens_per_block - 1) / p.tokens_per_block);
+    auto gob = [&](auto kernel) {
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      kernel<<<grid, 512, smem, st>>>(p, bh);
+    };
+    switch (loge5) {
+      case 0: gob(hash_bh_kernel<0>); break;
+      case 1: gob(hash_bh_kernel<1>); break;
+      case 2: gob(hash_bh_kernel<2>); break;
+      case 3: gob(hash_bh_kernel<3>); break;
+      case 4: gob(hash_bh_kernel<4>); break;
+      default: gob(hash_bh_kernel<5>); break;
+    }
+    ++c->launches;
+    LFFN_CUDA(cudaGetLastError());
+    return LFFN_OK;
+  }
   if (c->proj.kind == LFFN_PROJ_DENSE) {
     dim3 grid((unsigned)((c->code_width + 63) / 64), (unsigned)((n + 63) / 64));
     dense_proj_f64_kernel<<<grid, 256, 0, st>>>(d_x, c->d_W, c->d_zbuf, n, int(c->cfg.d_in),
@@ -492,8 +524,6 @@ int lffn_ctx_create_shard(lffn_ctx** out, int device, int64_t max_tokens, const 
   if (cfg->neighbor_count != 1)
     return fail(LFFN_ERR_USAGE,
                 "lookup forward: the device path implements the top-1 default (neighbor_count 1)");
-  if (proj->kind == LFFN_PROJ_BH)
-    return fail(LFFN_ERR_USAGE, "lookup forward: bh projection not yet on the device");
   if (max_tokens < 0) return fail(LFFN_ERR_USAGE, "ctx_create: negative max_tokens");
   if (table_end == 0 && table_begin == 0) table_end = cfg->tables;
   if (table_begin < 0 || table_end > cfg->tables || table_begin > table_end)
@@ -556,6 +586,11 @@ int lffn_ctx_create_shard(lffn_ctx** out, int device, int64_t max_tokens, const 
     c->n_transforms = int(2 * proj->depth);
     CK(cudaMalloc(&c->d_diag, size_t(2 * proj->depth * D) * sizeof(double)));
     CK(cudaMemcpy(c->d_diag, blob, size_t(2 * proj->depth * D) * sizeof(double), cudaMemcpyHostToDevice));
+  } else if (proj->kind == LFFN_PROJ_BH) {
+    c->n_transforms = int(proj->stages);
+    const size_t nb = size_t(blob_size(proj));
+    CK(cudaMalloc(&c->d_bh, nb * sizeof(double)));
+    CK(cudaMemcpy(c->d_bh, blob, nb * sizeof(double), cudaMemcpyHostToDevice));
   } else if (proj->kind == LFFN_PROJ_DENSE) {
     c->n_transforms = 0;
     const size_t nw = size_t(proj->d_in * proj->d_out);

@@ -33,8 +33,7 @@ def build(path):
                                                                      cfg.d_out, T)
 
 
-DEVICE_CASES = [p for p in GOLDEN
-                if int(np.load(p)["neighbor_count"]) == 1 and int(np.load(p)["kind"]) != 1]
+DEVICE_CASES = [p for p in GOLDEN if int(np.load(p)["neighbor_count"]) == 1]
 
 
 @pytest.mark.parametrize("path", DEVICE_CASES, ids=lambda p: os.path.basename(p)[:-4])

@@ -64,6 +64,35 @@ def test_hash_bit_exact(oracle, shape, kind):
     np.testing.assert_allclose(coeff, w_ref.astype(np.float32), rtol=2.5e-7, atol=0)
 
 
+BH_SHAPES = [
+    # d_in, d_out, h, tau, n, stages m, block b
+    (64, 64, 8, 4, 300, 2, 8),         # c1 width
+    (768, 768, 256, 8, 64, 4, 64),     # c2 width, the paper's BH4 b=64
+    (50, 30, 12, 10, 33, 4, 16),       # non-pow2 pad + truncate (D = 128)
+    (3, 5, 1, 2, 7, 1, 0),             # D = 4, one full-width block
+    (1024, 1024, 128, 10, 16, 4, 64),  # c3 width (truncating h*tau = 1280 of D = 2048)
+    (4096, 64, 512, 8, 6, 2, 32),      # D = 4096
+]
+
+
+@pytest.mark.parametrize("shape", BH_SHAPES, ids=lambda s: "x".join(map(str, s)))
+def test_hash_bh_bit_exact(oracle, shape):
+    """BH{m}: block-diagonal stages + Hadamard, z bit-identical."""
+    d_in, d_out, h, tau, n, m, b = shape
+    cfg, proj, T, x = _setup(d_in, d_out, h, tau, ProjKind.bh, n, stages=m, block=b)
+    layer = LookupFFN(cfg, proj, T, max_tokens=n)
+    codes, coeff, z = device_hash(layer, x)
+    c, s = to_oracle(cfg, proj)
+    z_ref = oracle.proj_forward(s, proj.blob, x.astype(np.float64))
+    assert np.array_equal(z.view(np.uint64), z_ref.view(np.uint64)), "z not bit-identical"
+    codes_ref, absz = oracle.compute_codes(z_ref, h, tau)
+    assert np.array_equal(codes, codes_ref)
+    y = device_forward(layer, x)
+    y_ref = oracle.lookup_forward(c, s, proj.blob, stored_tables(T.data, "f32"),
+                                  x.astype(np.float64))
+    assert_close(y, y_ref, FP32_TOL, "bh forward")
+
+
 def test_hash_scaled_variant(oracle):
     cfg, proj, T, x = _setup(64, 64, 16, 4, ProjKind.dense, 200, LookupVariant.scaled)
     layer = LookupFFN(cfg, proj, T, max_tokens=200)
