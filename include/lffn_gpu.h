@@ -184,6 +184,17 @@ int lffn_forward_host(lffn_ctx* ctx, const float* h_x, int64_t n, float* h_y);
  * check (status 2 with the stage named in lffn_last_error()). */
 int lffn_sync(lffn_ctx* ctx, void* stream);
 
+/* Context options:
+ *   LFFN_OPT_DENSE_EXACT       1 = dense projection in exact float64 (z
+ *                              bit-identical to projection.cpp:178-198);
+ *                              0 (default) = tcgen05 3xTF32 GEMM (codes exact
+ *                              wherever |z| > ~1e-5, BASELINE criterion)
+ *   LFFN_OPT_TABLE_GROUP_BYTES walk the tables in L2-sized groups of this many
+ *                              bytes (0 = one pass, the default) */
+#define LFFN_OPT_DENSE_EXACT 1
+#define LFFN_OPT_TABLE_GROUP_BYTES 2
+int lffn_ctx_set_option(lffn_ctx* ctx, int option, int64_t value);
+
 /* Number of kernels launched through this context since creation. */
 int64_t lffn_ctx_launch_count(const lffn_ctx* ctx);
 

@@ -16,6 +16,7 @@ LIB_PATH = os.path.join(HERE, "csrc", "liblffn_gpu.so")
 
 LFFN_OK, LFFN_ERR_USAGE, LFFN_ERR_NUMERIC, LFFN_ERR_RUNTIME = 0, 1, 2, 3
 LFFN_F32, LFFN_BF16, LFFN_F64 = 0, 1, 2
+LFFN_OPT_DENSE_EXACT, LFFN_OPT_TABLE_GROUP_BYTES = 1, 2
 
 
 class lffn_cfg(C.Structure):
@@ -62,6 +63,7 @@ SIGNATURES = {
     "lffn_forward": (C.c_int, [_VP, _VP, _I64, _VP, _VP]),
     "lffn_forward_host": (C.c_int, [_VP, _VP, _I64, _VP]),
     "lffn_sync": (C.c_int, [_VP, _VP]),
+    "lffn_ctx_set_option": (C.c_int, [_VP, C.c_int, _I64]),
     "lffn_ctx_launch_count": (_I64, [_VP]),
     "lffn_ctx_set_timing": (C.c_int, [_VP, C.c_int]),
     "lffn_ctx_stage_ms": (C.c_int, [_VP, C.POINTER(C.c_float), C.POINTER(C.c_float)]),

@@ -2,6 +2,8 @@
 // upload, and the stream-ordered launches of the hash (K1/K2) and gather (K3)
 // kernels.  No CPU compute path exists: every forward runs on the device and
 // a missing / failing CUDA runtime is reported as status 3.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -14,6 +16,7 @@
 
 #include "gather_kernels.cuh"
 #include "hash_kernels.cuh"
+#include "dense_tcgen05.cuh"
 #include "hash_bh_kernel.cuh"
 #include "hash_pair_kernel.cuh"
 #include "lffn_gpu.h"
@@ -55,6 +58,19 @@ struct lffn_ctx {
   double* d_diag = nullptr;
   double* d_W = nullptr;
   double* d_bh = nullptr;   // bh: m x (D/b) x b x b blocks (float64)
+  float* d_wt_hi = nullptr;  // dense (tcgen05): slice of W^T, tf32 hi / lo split
+  float* d_wt_lo = nullptr;
+  double* d_wt64 = nullptr;  // dense: slice of W^T in float64 (exact near-zero fixups)
+  int dense_ntile = 0;       // N tile of the tcgen05 dense GEMM (0: exact path only)
+  int dense_exact = 0;       // 1: exact float64 dense projection
+  alignas(64) CUtensorMap map_whi{}, map_wlo{}, map_xhi{}, map_xlo{};  // TMA maps (dense)
+  float* d_xhi = nullptr;  // dense: per-call tf32 hi / lo split of x (max_tokens x d_in)
+  float* d_xlo = nullptr;
+  uint2* d_fix_list = nullptr;  // dense tcgen05: deferred exact fixups
+  int* d_fix_count = nullptr;
+  int fix_cap = 0;
+  long long* d_dense_prof = nullptr;  // LFFN_DENSE_PROF: per-CTA timestamps (debug)
+  int64_t dense_prof_len = 0;
   double* d_zbuf = nullptr;  // dense: [max_tokens x code_width] float64
 
   // tables
@@ -120,6 +136,23 @@ void destroy_ctx(lffn_ctx* c) {
   cudaFree(c->d_diag);
   cudaFree(c->d_W);
   cudaFree(c->d_bh);
+  cudaFree(c->d_wt_hi);
+  cudaFree(c->d_wt_lo);
+  cudaFree(c->d_wt64);
+  cudaFree(c->d_xhi);
+  cudaFree(c->d_xlo);
+  cudaFree(c->d_fix_list);
+  cudaFree(c->d_fix_count);
+  if (c->d_dense_prof) {
+    // debug dump: [cta][start, mainloop done, end, smid] globaltimer ns
+    std::vector<long long> h(size_t(c->dense_prof_len));
+    cudaMemcpy(h.data(), c->d_dense_prof, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
+    if (FILE* f = fopen(getenv("LFFN_DENSE_PROF"), "wb")) {
+      fwrite(h.data(), sizeof(long long), h.size(), f);
+      fclose(f);
+    }
+    cudaFree(c->d_dense_prof);
+  }
   cudaFree(c->d_zbuf);
   cudaFree(c->d_T_owned);
   cudaFree(c->d_codes);
@@ -139,6 +172,65 @@ void destroy_ctx(lffn_ctx* c) {
   if (c->ev_t1) cudaEventDestroy(c->ev_t1);
   if (c->ev_t2) cudaEventDestroy(c->ev_t2);
   delete c;
+}
+
+// 2-D fp32 TMA map (inner dimension contiguous), SWIZZLE_128B boxes of
+// box_inner x box_outer, zero fill out of bounds.
+// tau values whose lcm(tau, 16) <= 128 (the tcgen05 path's N tile holds whole tables)
+template <int TAU>
+void launch_dense_tau(dim3 grid, size_t smem, cudaStream_t st, const CUtensorMap& a,
+                      const CUtensorMap& b, const CUtensorMap& c, const CUtensorMap& d,
+                      const DenseParams& p) {
+  static bool attr = [&] {
+    cudaFuncSetAttribute(dense_tcgen05_kernel<TAU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(dense_smem_bytes(128)));
+    return true;
+  }();
+  (void)attr;
+  dense_tcgen05_kernel<TAU><<<grid, 128, smem, st>>>(a, b, c, d, p);
+}
+
+int launch_dense_tcgen05(int tau, dim3 grid, size_t smem, cudaStream_t st, const CUtensorMap& a,
+                         const CUtensorMap& b, const CUtensorMap& c, const CUtensorMap& d,
+                         const DenseParams& p) {
+  switch (tau) {
+#define LFFN_TAU(T) \
+  case T:           \
+    launch_dense_tau<T>(grid, smem, st, a, b, c, d, p); \
+    return LFFN_OK;
+    LFFN_TAU(1) LFFN_TAU(2) LFFN_TAU(3) LFFN_TAU(4) LFFN_TAU(5) LFFN_TAU(6) LFFN_TAU(7)
+    LFFN_TAU(8) LFFN_TAU(10) LFFN_TAU(12) LFFN_TAU(14) LFFN_TAU(16) LFFN_TAU(20) LFFN_TAU(24)
+#undef LFFN_TAU
+    default:
+      return fail(LFFN_ERR_USAGE, "dense tcgen05: unsupported code_bits " + std::to_string(tau));
+  }
+}
+
+int make_tma_map(CUtensorMap* map, const float* base, uint64_t inner, uint64_t outer,
+                 uint32_t box_inner, uint32_t box_outer) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (!encode) return fail(LFFN_ERR_RUNTIME, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {inner, std::max<uint64_t>(outer, 1)};
+  const cuuint64_t strides[1] = {inner * sizeof(float)};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
+                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            box_inner * sizeof(float) == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                            : CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(LFFN_ERR_RUNTIME, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+  return LFFN_OK;
 }
 
 int check_n(const lffn_ctx* c, int64_t n) {
@@ -198,6 +290,63 @@ int launch_hash(lffn_ctx* c, const float* d_x, int64_t n, uint32_t* codes, float
       case 4: gob(hash_bh_kernel<4>); break;
       default: gob(hash_bh_kernel<5>); break;
     }
+    ++c->launches;
+    LFFN_CUDA(cudaGetLastError());
+    return LFFN_OK;
+  }
+  if (c->proj.kind == LFFN_PROJ_DENSE && !c->dense_exact && c->dense_ntile > 0) {
+    // tcgen05 3xTF32 GEMM fused with codes / coefficients (dense_tcgen05.cuh)
+    DenseParams d{};
+    d.x = d_x;
+    d.wt_hi = c->d_wt_hi;
+    d.wt_lo = c->d_wt_lo;
+    d.wt64 = c->d_wt64;
+    d.n = n;
+    d.d_in = int(c->cfg.d_in);
+    d.col_begin = int(c->kb * c->cfg.code_bits);
+    d.ncols = int(c->h_loc * c->cfg.code_bits);
+    d.ntile = c->dense_ntile;
+    d.tau = int(c->cfg.code_bits);
+    d.scaled = p.scaled;
+    d.z_out = z_out;
+    d.code_width = int(c->code_width);
+    d.codes = codes;
+    d.coeff = coeff;
+    d.flag = c->d_flag;
+    static const float fix = getenv("LFFN_DENSE_FIXUP") ? float(atof(getenv("LFFN_DENSE_FIXUP"))) : kDenseFixup;
+    d.fixup = fix;
+    d.fix_list = c->d_fix_list;
+    d.fix_count = c->d_fix_count;
+    d.fix_cap = c->fix_cap;
+    // split x into tf32 hi / lo (ctx scratch; the TMA maps are built once)
+    const int64_t cnt = n * c->cfg.d_in;
+    dense_split_x_kernel<<<unsigned(std::min<int64_t>(int64_t(c->num_sms) * 8, (cnt / 4 + 255) / 256 + 1)),
+                           256, 0, st>>>(d_x, cnt, c->d_xhi, c->d_xlo, c->d_flag, c->d_fix_count);
+    ++c->launches;
+    const size_t smem = dense_smem_bytes(d.ntile);
+
+    dim3 grid((unsigned)((d.ncols + d.ntile - 1) / d.ntile), (unsigned)((n + umma::BM - 1) / umma::BM));
+    if (getenv("LFFN_DENSE_PROF")) {
+      const int64_t len = int64_t(grid.x) * grid.y * 4;
+      if (len > c->dense_prof_len) {
+        cudaFree(c->d_dense_prof);
+        cudaMalloc(&c->d_dense_prof, size_t(len) * sizeof(long long));
+        c->dense_prof_len = len;
+      }
+      d.prof = c->d_dense_prof;
+    }
+    const int rc = launch_dense_tcgen05(int(c->cfg.code_bits), grid, smem, st, c->map_xhi, c->map_xlo,
+                                        c->map_whi, c->map_wlo, d);
+    if (rc != LFFN_OK) return rc;
+    ++c->launches;
+    // exact fixups: d_in <= 6144 keeps the per-warp product rows in 192 KB
+    const size_t fsm = size_t(kFixupWarps) * size_t(d.d_in) * sizeof(double);
+    static bool fattr = [] {
+      cudaFuncSetAttribute(dense_fixup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      return true;
+    }();
+    (void)fattr;
+    dense_fixup_kernel<<<unsigned(c->num_sms), 32 * kFixupWarps, fsm, st>>>(d);
     ++c->launches;
     LFFN_CUDA(cudaGetLastError());
     return LFFN_OK;
@@ -597,6 +746,46 @@ int lffn_ctx_create_shard(lffn_ctx** out, int device, int64_t max_tokens, const 
     CK(cudaMalloc(&c->d_W, nw * sizeof(double)));
     CK(cudaMemcpy(c->d_W, blob, nw * sizeof(double), cudaMemcpyHostToDevice));
     CK(cudaMalloc(&c->d_zbuf, size_t(std::max<int64_t>(max_tokens, 1)) * c->code_width * sizeof(double)));
+    // tcgen05 3xTF32 path: N tile = largest multiple of lcm(tau, 16) <= 256
+    int64_t l = 16;
+    while (l % cfg->code_bits != 0) l += 16;
+    const int64_t ncols = c->h_loc * cfg->code_bits;
+    if (l <= 128 && ncols > 0 && proj->d_in % 4 == 0 && proj->d_in <= 6144) {
+      // N <= 128 so the kSegs K-segment accumulators fit kTmemCols (two CTAs per SM)
+      c->dense_ntile = int((128 / l) * l);
+      const size_t nw = size_t(ncols) * size_t(proj->d_in);
+      CK(cudaMalloc(&c->d_wt_hi, nw * sizeof(float)));
+      CK(cudaMalloc(&c->d_wt_lo, nw * sizeof(float)));
+      CK(cudaMalloc(&c->d_wt64, nw * sizeof(double)));
+      dense_split_weights_kernel<<<unsigned((nw + 255) / 256), 256>>>(
+          c->d_W, int(proj->d_in), int(c->code_width), int(c->kb * cfg->code_bits), int(ncols),
+          c->d_wt_hi, c->d_wt_lo, c->d_wt64);
+      CK(cudaGetLastError());
+      CK(cudaDeviceSynchronize());
+      if (make_tma_map(&c->map_whi, c->d_wt_hi, uint64_t(proj->d_in), uint64_t(ncols), umma::BK,
+                       uint32_t(c->dense_ntile)) ||
+          make_tma_map(&c->map_wlo, c->d_wt_lo, uint64_t(proj->d_in), uint64_t(ncols), umma::BK,
+                       uint32_t(c->dense_ntile)))
+        c->dense_ntile = 0;  // no TMA encoder: exact float64 path
+      if (c->dense_ntile > 0) {
+        const size_t nx = size_t(std::max<int64_t>(max_tokens, 1)) * size_t(proj->d_in);
+        CK(cudaMalloc(&c->d_xhi, nx * sizeof(float)));
+        CK(cudaMalloc(&c->d_xlo, nx * sizeof(float)));
+        // |z| < 1e-4 is ~1e-4 of the z for Gaussian-like projections; 1M
+        // entries (8 MB) covers 4096 x 2048 all-candidate tiles before the
+        // kernel falls back to inline recomputation
+        c->fix_cap = 1 << 20;
+        CK(cudaMalloc(&c->d_fix_list, size_t(c->fix_cap) * sizeof(uint2)));
+        CK(cudaMalloc(&c->d_fix_count, sizeof(int)));
+        CK(cudaMemset(c->d_fix_count, 0, sizeof(int)));
+        if (make_tma_map(&c->map_xhi, c->d_xhi, uint64_t(proj->d_in), uint64_t(std::max<int64_t>(max_tokens, 1)),
+                         umma::BK, umma::BM) ||
+            make_tma_map(&c->map_xlo, c->d_xlo, uint64_t(proj->d_in), uint64_t(std::max<int64_t>(max_tokens, 1)),
+                         umma::BK, umma::BM))
+          c->dense_ntile = 0;
+      }
+    }
+    if (const char* e = getenv("LFFN_DENSE_EXACT")) c->dense_exact = atoi(e);
   }
 
   const size_t mt = size_t(std::max<int64_t>(max_tokens, 1));
@@ -756,6 +945,20 @@ int lffn_sync(lffn_ctx* c, void* stream) {
   if (!c) return fail(LFFN_ERR_USAGE, "null context");
   DeviceGuard g(c->device);
   return read_flag(c, static_cast<cudaStream_t>(stream));
+}
+
+int lffn_ctx_set_option(lffn_ctx* c, int option, int64_t value) {
+  if (!c) return fail(LFFN_ERR_USAGE, "null context");
+  switch (option) {
+    case LFFN_OPT_DENSE_EXACT:
+      c->dense_exact = value != 0;
+      return LFFN_OK;
+    case LFFN_OPT_TABLE_GROUP_BYTES:
+      if (value < 0) return fail(LFFN_ERR_USAGE, "option: negative table group size");
+      c->table_group_bytes = size_t(value);
+      return LFFN_OK;
+  }
+  return fail(LFFN_ERR_USAGE, "option: unknown option " + std::to_string(option));
 }
 
 int lffn_ctx_set_timing(lffn_ctx* c, int enable) {

@@ -390,6 +390,13 @@ class LookupFFN:
     def forward_host_ptr(self, x_ptr: int, n: int, y_ptr: int) -> None:
         check(_capi.lib().lffn_forward_host(self._ctx, x_ptr, n, y_ptr))
 
+    def set_option(self, name: str, value: int) -> None:
+        """'dense_exact' (exact float64 dense projection instead of the
+        tcgen05 3xTF32 GEMM) or 'table_group_bytes'."""
+        opt = {"dense_exact": _capi.LFFN_OPT_DENSE_EXACT,
+               "table_group_bytes": _capi.LFFN_OPT_TABLE_GROUP_BYTES}[name]
+        check(_capi.lib().lffn_ctx_set_option(self._ctx, opt, int(value)))
+
     def launch_count(self) -> int:
         return int(_capi.lib().lffn_ctx_launch_count(self._ctx))
 

@@ -33,6 +33,10 @@ def build(path):
                                                                      cfg.d_out, T)
 
 
+def cfg_is_dense(d) -> bool:
+    return ProjKind(int(d["kind"])) == ProjKind.dense
+
+
 DEVICE_CASES = [p for p in GOLDEN if int(np.load(p)["neighbor_count"]) == 1]
 
 
@@ -42,6 +46,16 @@ def test_device_matches_reference_fixture(path):
     x = d["x"].astype(np.float32)
     assert np.array_equal(x.astype(np.float64), d["x"])  # fixture inputs are fp32 values
     layer = LookupFFN(cfg, proj, T, max_tokens=x.shape[0])
+    if cfg_is_dense(d):
+        # default dense path = tcgen05 3xTF32: z within 1e-4, exact near zero,
+        # codes bit-exact, y at the fp32 bar
+        codes, coeff, z = device_hash(layer, x)
+        assert np.max(np.abs(z - d["z"])) <= 1e-4 * max(1.0, np.max(np.abs(d["z"])))
+        small = np.abs(z) < 1e-4
+        assert np.array_equal(z[small].view(np.uint64), d["z"][small].view(np.uint64))
+        assert np.array_equal(codes, d["codes"][..., 0])
+        assert_close(device_forward(layer, x), d["y"], 1e-5, os.path.basename(path) + " tcgen05")
+        layer.set_option("dense_exact", 1)  # then the bit-exact float64 projection below
     codes, coeff, z = device_hash(layer, x)
     assert np.array_equal(z.view(np.uint64), d["z"].view(np.uint64)), "z vs reference"
     assert np.array_equal(codes, d["codes"][..., 0])
