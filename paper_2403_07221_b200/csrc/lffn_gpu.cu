@@ -85,8 +85,8 @@ struct lffn_ctx {
   int* h_flag = nullptr;  // pinned
   float* d_xbuf = nullptr;
   float* d_ybuf = nullptr;
-  cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
-  static constexpr int kChunks = 8;
+  cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_comp2 = nullptr, s_d2h = nullptr;
+  static constexpr int kChunks = 16;
   cudaEvent_t ev_h2d[kChunks] = {}, ev_comp[kChunks] = {};
   cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr, ev_t2 = nullptr;
   bool timing = false;
@@ -163,6 +163,7 @@ void destroy_ctx(lffn_ctx* c) {
   cudaFree(c->d_ybuf);
   if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
   if (c->s_comp) cudaStreamDestroy(c->s_comp);
+  if (c->s_comp2) cudaStreamDestroy(c->s_comp2);
   if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
   for (int i = 0; i < lffn_ctx::kChunks; ++i) {
     if (c->ev_h2d[i]) cudaEventDestroy(c->ev_h2d[i]);
@@ -482,13 +483,15 @@ int launch_gather_group(lffn_ctx* c, const uint32_t* codes, const float* coeff, 
       const int64_t pwarps = n * pwpt;
       const unsigned pgrid = (unsigned)std::min<int64_t>(int64_t(c->num_sms) * 2, (pwarps * 32 + 255) / 256);
       (void)pg;
+      // (measured at c2 fp32: one warp per token with 6 chunks and 2 CTAs/SM
+      // beats 2-3 warps per token at 3-4 CTAs/SM, 0.641 vs 0.698-0.942 ms;
+      // L2 evict_last/evict_first splits of the table stack: 0.68-0.81 ms)
 #define LFFN_PROW(TT, M, TIF) gather_row_persistent_kernel<TT, M, TIF, 2><<<pgrid, 256, 0, st>>>(p, pwpt);
       if (f32) {
         if (pmaxc == 2) { LFFN_PROW(float, 2, 4) } else if (pmaxc == 4) { LFFN_PROW(float, 4, 4) }
         else { LFFN_PROW(float, 6, 4) }
       } else {
-        if (pmaxc == 2) { LFFN_PROW(__nv_bfloat16, 2, 4) } else if (pmaxc == 3) { LFFN_PROW(__nv_bfloat16, 3, 4) }
-        else { LFFN_PROW(__nv_bfloat16, 4, 4) }
+        if (pmaxc == 2) { LFFN_PROW(__nv_bfloat16, 2, 4) } else if (pmaxc == 3) { LFFN_PROW(__nv_bfloat16, 3, 4) } else { LFFN_PROW(__nv_bfloat16, 4, 4) }
       }
 #undef LFFN_PROW
       ++c->launches;
@@ -796,6 +799,7 @@ int lffn_ctx_create_shard(lffn_ctx** out, int device, int64_t max_tokens, const 
   CK(cudaMallocHost(&c->h_flag, sizeof(int)));
   CK(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&c->s_comp2, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
   for (int i = 0; i < lffn_ctx::kChunks; ++i) {
     CK(cudaEventCreateWithFlags(&c->ev_h2d[i], cudaEventDisableTiming));
@@ -917,23 +921,30 @@ int lffn_forward_host(lffn_ctx* c, const float* h_x, int64_t n, float* h_y) {
   }
   if (n == 0) return LFFN_OK;
   // Chunked pipeline: H2D(chunk i+1) || compute(chunk i) || D2H(chunk i-1).
+  // Structured projections use no context scratch, so consecutive chunks
+  // alternate between two compute streams and their kernels overlap (one
+  // chunk alone does not fill the GPU); the dense kind keeps one stream (its
+  // split-x / fixup scratch is per context).
   const int64_t d_in = c->cfg.d_in, d_out = c->cfg.d_out;
-  int nch = int(std::min<int64_t>(lffn_ctx::kChunks, std::max<int64_t>(1, n / 1024)));
+  static const int want = getenv("LFFN_HOST_CHUNKS") ? atoi(getenv("LFFN_HOST_CHUNKS")) : 8;
+  int nch = int(std::min<int64_t>(std::min(want, lffn_ctx::kChunks), std::max<int64_t>(1, n / 512)));
+  const bool dual = c->proj.kind != LFFN_PROJ_DENSE;
   const int64_t per = (n + nch - 1) / nch;
   for (int i = 0; i < nch; ++i) {
     const int64_t r0 = i * per, r1 = std::min(n, r0 + per);
     if (r0 >= r1) break;
+    cudaStream_t sc = (dual && (i & 1)) ? c->s_comp2 : c->s_comp;
     LFFN_CUDA(cudaMemcpyAsync(c->d_xbuf + r0 * d_in, h_x + r0 * d_in,
                               size_t(r1 - r0) * d_in * sizeof(float), cudaMemcpyHostToDevice, c->s_h2d));
     LFFN_CUDA(cudaEventRecord(c->ev_h2d[i], c->s_h2d));
-    LFFN_CUDA(cudaStreamWaitEvent(c->s_comp, c->ev_h2d[i], 0));
+    LFFN_CUDA(cudaStreamWaitEvent(sc, c->ev_h2d[i], 0));
     if (int rc = launch_hash(c, c->d_xbuf + r0 * d_in, r1 - r0, c->d_codes + r0 * c->h_loc,
-                             c->d_coeff + r0 * c->h_loc, nullptr, c->s_comp))
+                             c->d_coeff + r0 * c->h_loc, nullptr, sc))
       return rc;
     if (int rc = launch_gather(c, c->d_codes + r0 * c->h_loc, c->d_coeff + r0 * c->h_loc, r1 - r0,
-                               c->d_ybuf + r0 * d_out, 0, c->s_comp))
+                               c->d_ybuf + r0 * d_out, 0, sc))
       return rc;
-    LFFN_CUDA(cudaEventRecord(c->ev_comp[i], c->s_comp));
+    LFFN_CUDA(cudaEventRecord(c->ev_comp[i], sc));
     LFFN_CUDA(cudaStreamWaitEvent(c->s_d2h, c->ev_comp[i], 0));
     LFFN_CUDA(cudaMemcpyAsync(h_y + r0 * d_out, c->d_ybuf + r0 * d_out,
                               size_t(r1 - r0) * d_out * sizeof(float), cudaMemcpyDeviceToHost, c->s_d2h));
