@@ -68,7 +68,7 @@ typedef struct lffn_cfg {
   int64_t tables;         /* h */
   int64_t code_bits;      /* tau */
   int32_t variant;        /* LFFN_SOFTMAX .. LFFN_GELU_TAU1 */
-  int32_t neighbor_count; /* nc; the device path implements nc == 1 */
+  int32_t neighbor_count; /* nc; the device path implements 1 <= nc <= 256 */
 } lffn_cfg;
 
 /* ProjectionSpec + Projection::blob() (projection.hpp:21-95).  blob is a
@@ -159,19 +159,24 @@ int lffn_ctx_create_from_checkpoint(lffn_ctx** out, int device, int64_t max_toke
 /* Hash stage = Projection::forward (projection.cpp:167-266) + compute_codes
  * (lookup.cpp:81-100) + top-1 weight (lookup.cpp:185-189), i.e. the
  * lookup_hash_f32 + lookup_weights_f32 pair (bench.cpp:115-180), in one
- * kernel.  d_codes/d_coeff: [n x h_local]; d_z (optional, may be NULL):
- * [n x h*tau] float64 projection output (bit-identical to the reference's
- * double Projection::forward for the signflip kind). */
+ * kernel.  d_codes/d_coeff: [n x h_local x nc]; for nc > 1 the records of a
+ * (token, table) are neighbor_codes (lookup.cpp:118-165) in the reference's
+ * order with coefficient exp(<z,S_c> - logden) (x <z,S_c> when scaled,
+ * lookup.cpp:241-252), the LookupCache slot layout (i*h + k)*nc + c.
+ * d_z (optional, may be NULL): [n x h*tau] float64 projection output
+ * (bit-identical to the reference's double Projection::forward for the
+ * signflip, acdc, bh and exact-dense kinds). */
 int lffn_hash(lffn_ctx* ctx, const float* d_x, int64_t n, uint32_t* d_codes, float* d_coeff,
               double* d_z, void* stream);
 
 /* Gather stage = lookup_gather_f32 (bench.cpp:182-194): y_i (+)= sum_k
- * coeff[i,k] * T[k][codes[i,k]], tables in ascending order.  accumulate = 0
+ * coeff[i,k] * T[k][codes[i,k]], tables in ascending order (nc > 1: records
+ * (k, c) in slot order, forward_impl lookup.cpp:238-262).  accumulate = 0
  * overwrites y (the reference zero-fills first), 1 adds into y. */
 int lffn_lookup_accumulate(lffn_ctx* ctx, const uint32_t* d_codes, const float* d_coeff,
                            int64_t n, float* d_y, int accumulate, void* stream);
 
-/* Full forward = lookup_forward (lookup.cpp:191-282) for nc == 1:
+/* Full forward = lookup_forward (lookup.cpp:191-282):
  * hash -> gather on the device, no host round trip. */
 int lffn_forward(lffn_ctx* ctx, const float* d_x, int64_t n, float* d_y, void* stream);
 

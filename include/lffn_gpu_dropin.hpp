@@ -14,8 +14,8 @@
 // projection.hpp, matrix.hpp, common.hpp) for DenseMatrix / Projection /
 // HashTables / LookupConfig and the error types; nothing here depends on the
 // reference's implementation files.  There is no CPU fallback: a missing
-// device surfaces as std::runtime_error, a LookupCache (training) or
-// neighbor_count > 1 as UsageError.
+// device surfaces as std::runtime_error, a LookupCache (training) as
+// UsageError, neighbor_count above the device limit (256) as SizeError.
 #pragma once
 
 #include <memory>
@@ -72,8 +72,6 @@ class Layer {
   Layer(const Projection& proj, const HashTables& tables, const LookupConfig& cfg,
         std::size_t max_tokens, int device = 0, bool bf16_tables = false)
       : cfg_(cfg) {
-    if (cfg.neighbor_count != 1)
-      throw UsageError("lffn::gpu: the device path implements the top-1 default");
     const lffn_cfg c = to_c(cfg);
     const lffn_proj p = to_c(proj);
     lffn_ctx* ctx = nullptr;
@@ -106,7 +104,7 @@ class Layer {
   std::unique_ptr<lffn_ctx, Deleter> ctx_;
 };
 
-/// Drop-in for lffn::lookup_forward (lookup.hpp:124-125), top-1 only.
+/// Drop-in for lffn::lookup_forward (lookup.hpp:124-125), any neighbor_count <= 256.
 inline DenseMatrix lookup_forward(const DenseMatrix& x, const Projection& proj,
                                   const HashTables& tables, const LookupConfig& cfg,
                                   LookupCache* cache = nullptr) {

@@ -90,6 +90,55 @@ int main() {
         EXPECT(std::abs(y.at(i, j) - expected) <= 1e-6 * std::abs(expected) + 1e-9, "zero proj");
       }
   }
+  // neighbor_count > 1 (lookup.cpp:118-165, 231-262) against the reference
+  {
+    LookupConfig n3{.d_in = 64, .d_out = 64, .tables = 8, .code_bits = 4, .neighbor_count = 3};
+    parity_case("c1 signflip nc=3", n3, ProjectionSpec::signflip(64, 32), 512, 0, 0.02);
+    LookupConfig n5{.d_in = 50, .d_out = 30, .tables = 12, .code_bits = 10,
+                    .variant = LookupVariant::scaled, .neighbor_count = 5};
+    parity_case("scaled nc=5 pad+truncate", n5, ProjectionSpec::signflip(50, 120), 33, 5, 0.02);
+    LookupConfig n4{.d_in = 64, .d_out = 64, .tables = 8, .code_bits = 4, .neighbor_count = 4};
+    parity_case("dense nc=4", n4, ProjectionSpec::dense(64, 32), 128, 3, 0.02);
+  }
+  // test_lookup.cpp:251-272 -- full-neighbour forward (nc = 2^tau), bh, both variants
+  for (LookupVariant variant : {LookupVariant::softmax, LookupVariant::scaled}) {
+    LookupConfig cfg{.d_in = 8, .d_out = 6, .tables = 2, .code_bits = 3, .variant = variant,
+                     .neighbor_count = 8};
+    parity_case(variant == LookupVariant::softmax ? "full codebook softmax" : "full codebook scaled",
+                cfg, ProjectionSpec::bh(8, 6, 2, 4), 16, 33, 0.5);
+  }
+  // test_lookup.cpp:274-342 -- tau = 1 sigmoid / GELU constructions (nc = 2)
+  for (LookupVariant variant : {LookupVariant::sigmoid_tau1, LookupVariant::gelu_tau1}) {
+    const std::size_t d = 7, units = 9, d_out = 4;
+    auto rng = make_rng(36);
+    const DenseMatrix w = DenseMatrix::gaussian(units, d, rng);
+    const DenseMatrix v = DenseMatrix::gaussian(units, d_out, rng);
+    LookupConfig cfg{.d_in = d, .d_out = d_out, .tables = units, .code_bits = 1,
+                     .variant = variant, .neighbor_count = 2};
+    const double sw = variant == LookupVariant::sigmoid_tau1 ? 0.5 : 0.851;
+    const double sv = variant == LookupVariant::sigmoid_tau1 ? 1.0 : 1.175;
+    std::vector<double> blob(d * units);
+    for (std::size_t k = 0; k < units; ++k)
+      for (std::size_t c = 0; c < d; ++c) blob[c * units + k] = sw * w.at(k, c);
+    Projection proj = Projection::from_blob(ProjectionSpec::dense(d, units), blob);
+    HashTables tables = HashTables::zeros_like(cfg);
+    for (std::size_t k = 0; k < units; ++k)
+      for (std::size_t j = 0; j < d_out; ++j) tables.row(k, 1)[j] = double(float(sv * v.at(k, j)));
+    DenseMatrix x = DenseMatrix::gaussian(12, d, rng);
+    round_to_f32(x);
+    const DenseMatrix y_ref = lookup_forward(x, proj, tables, cfg);
+    const DenseMatrix y_gpu = gpu::lookup_forward(x, proj, tables, cfg);
+    const double e1 = l2_rel(y_gpu, y_ref), e2 = maxabs_rel(y_gpu, y_ref);
+    std::printf("%-28s l2_rel=%.2e maxabs_rel=%.2e\n",
+                variant == LookupVariant::sigmoid_tau1 ? "tau1 sigmoid nc=2" : "tau1 gelu nc=2", e1, e2);
+    EXPECT(e1 <= 1e-5 && e2 <= 1e-5, "tau1 construction parity");
+    if (variant == LookupVariant::gelu_tau1) {
+      // GELU(0) = 0: the scaled numerator zeroes at z = 0
+      const DenseMatrix zeros(3, d);
+      const DenseMatrix y0 = gpu::lookup_forward(zeros, proj, tables, cfg);
+      for (double val : y0.data) EXPECT(val == 0.0, "gelu(0) == 0");
+    }
+  }
   // test_lookup.cpp:232-249 -- tau = 1 with equal rows halves the sum
   {
     LookupConfig cfg{.d_in = 4, .d_out = 3, .tables = 5, .code_bits = 1};

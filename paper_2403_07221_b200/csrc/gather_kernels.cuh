@@ -4,12 +4,12 @@
 // forward_impl (lookup.cpp:223-268).  Tables are walked in ascending order
 // with fp32 accumulators in registers, as the reference's f32 path does.
 //
-// This file holds the direct-gather kernel: each warp owns NTOK tokens x one
-// column chunk of 32*VEC columns and reads every gathered row segment with
-// 128-bit loads straight from L2 (the L2-resident table working set keeps
-// the HBM traffic at the unique bytes).  It serves every shape; the staged
-// kernel in staged_gather.cuh beats the L2 roofline for tables whose row
-// count is small enough to stage.
+// Kernels: gather_row_persistent_kernel (the default: one warp per token or
+// part of its row, persistent grid, several tables' 128-bit row segments in
+// flight per lane), gather_row_kernel (same without the 4-record layout) and
+// gather_direct_kernel (any width; NTOK tokens x one column chunk per warp).
+// Records are (table, neighbour) pairs, table-major: with neighbor_count nc
+// record r reads table r / nc (nc = 1 is the top-1 default).
 #pragma once
 
 #include <cstdint>
@@ -31,7 +31,13 @@ struct GatherParams {
   int accumulate;
   int* flag;
   int reverse_odd_rounds;   // persistent kernel: odd rounds walk the tables backwards
+  int nc;                   // records per table (neighbor_count): record r reads table r / nc
 };
+
+// table of record r (records are (table, neighbour) pairs, table-major)
+__device__ __forceinline__ int64_t rec_table(const GatherParams& p, int r) {
+  return p.nc == 1 ? r : r / p.nc;
+}
 
 template <typename TT, int VEC>
 struct RowLoad;
@@ -105,7 +111,7 @@ __global__ void __launch_bounds__(256) gather_direct_kernel(GatherParams p) {
       if (t < ntok) {
         const uint32_t code = __ldg(cbase + (int64_t)t * p.ld + k);
         w[t] = __ldg(wbase + (int64_t)t * p.ld + k);
-        if (colok) RowLoad<TT, VEC>::load(T + k * table_stride + (int64_t)code * p.d_out + col, vals[t]);
+        if (colok) RowLoad<TT, VEC>::load(T + rec_table(p, k) * table_stride + (int64_t)code * p.d_out + col, vals[t]);
       }
     }
 #pragma unroll
@@ -162,7 +168,7 @@ __global__ void __launch_bounds__(256) gather_row_kernel(GatherParams p, int war
     for (int v = 0; v < VEC; ++v) acc[c][v] = 0.f;
 
   auto row_loads = [&](int k, uint32_t code, float (&vals)[MAXC][VEC]) {
-    const TT* rp = T + k * tstride + (int64_t)code * p.d_out + colbase;
+    const TT* rp = T + rec_table(p, k) * tstride + (int64_t)code * p.d_out + colbase;
 #pragma unroll
     for (int c = 0; c < MAXC; ++c) {
       if (c < nck && colbase + c * CHUNK < p.d_out) RowLoad<TT, VEC>::load(rp + c * CHUNK, vals[c]);
@@ -326,7 +332,7 @@ __global__ void __launch_bounds__(256, MINB) gather_row_persistent_kernel(Gather
         uint4 raw[TIF][MAXC];
 #pragma unroll
         for (int q = 0; q < TIF; ++q) {
-          const TT* rp = T + (kg + q0 + q) * tstride + (int64_t)codes4[q0 + q] * p.d_out + colbase;
+          const TT* rp = T + rec_table(p, kg + q0 + q) * tstride + (int64_t)codes4[q0 + q] * p.d_out + colbase;
 #pragma unroll
           for (int c = 0; c < MAXC; ++c)
             raw[q][c] = ok[c] ? Raw<TT>::load(rp + c * CHUNK) : make_uint4(0u, 0u, 0u, 0u);

@@ -21,7 +21,7 @@
 #include "hash_pair_kernel.cuh"
 #include "lffn_gpu.h"
 #include "lffn_internal.h"
-#include "staged_gather.cuh"
+#include "neighbor_kernels.cuh"
 
 namespace lffn_gpu {
 
@@ -51,6 +51,7 @@ struct lffn_ctx {
   lffn_cfg cfg{};
   lffn_proj proj{};  // blob pointer cleared after the copy
   int64_t D = 1, logD = 0, code_width = 0, rows = 0, kb = 0, ke = 0, h_loc = 0;
+  int64_t nc = 1;  // neighbor_count: records per (token, table)
   int n_transforms = 0;
 
   // projection parameters on the device
@@ -93,8 +94,6 @@ struct lffn_ctx {
   bool timed = false;
 
   int64_t launches = 0;
-  int staged_ok = 0;
-  int staged_smem = 0;
   int num_sms = 148;
   size_t table_group_bytes = 0;  // >0: walk tables in groups of this many bytes (measured slower on c2)
 };
@@ -245,8 +244,47 @@ int check_n(const lffn_ctx* c, int64_t n) {
 
 // ---------------------------------------------------------------- launches
 
+int launch_hash_top1(lffn_ctx* c, const float* d_x, int64_t n, uint32_t* codes, float* coeff,
+                     double* z_out, cudaStream_t st, bool exact_z);
+
+// Hash stage.  nc == 1: codes / coefficients of the top-1 code.  nc > 1: the
+// projection writes z (float64, exact: the dense kind takes the float64
+// kernel so neighbour ORDER follows the reference's |z|), then one thread per
+// (token, table) enumerates the nc neighbour codes and their coefficients
+// (neighbor_kernels.cuh); codes / coeff are [n][h_loc][nc].
 int launch_hash(lffn_ctx* c, const float* d_x, int64_t n, uint32_t* codes, float* coeff,
                 double* z_out, cudaStream_t st) {
+  if (c->nc == 1) return launch_hash_top1(c, d_x, n, codes, coeff, z_out, st, false);
+  if (n == 0) return LFFN_OK;
+  double* z = z_out ? z_out : c->d_zbuf;
+  // the top-1 outputs of the projection kernel land in the first n*h_loc
+  // records and are overwritten below
+  if (int rc = launch_hash_top1(c, d_x, n, codes, coeff, z, st, true)) return rc;
+  if (c->h_loc == 0) return LFFN_OK;
+  NeighborParams q{};
+  q.z = z;
+  q.n = n;
+  q.code_width = int(c->code_width);
+  q.tau = int(c->cfg.code_bits);
+  q.kb = int(c->kb);
+  q.ke = int(c->ke);
+  q.nc = int(c->nc);
+  q.scaled = (c->cfg.variant == LFFN_SCALED || c->cfg.variant == LFFN_GELU_TAU1) ? 1 : 0;
+  q.codes = codes;
+  q.coeff = coeff;
+  q.flag = c->d_flag;
+  const unsigned grid = unsigned((n * c->h_loc + 127) / 128);
+  if (c->nc <= 4) neighbor_kernel<4><<<grid, 128, 0, st>>>(q);
+  else if (c->nc <= 16) neighbor_kernel<16><<<grid, 128, 0, st>>>(q);
+  else if (c->nc <= 64) neighbor_kernel<64><<<grid, 128, 0, st>>>(q);
+  else neighbor_kernel<256><<<grid, 128, 0, st>>>(q);
+  ++c->launches;
+  LFFN_CUDA(cudaGetLastError());
+  return LFFN_OK;
+}
+
+int launch_hash_top1(lffn_ctx* c, const float* d_x, int64_t n, uint32_t* codes, float* coeff,
+                     double* z_out, cudaStream_t st, bool exact_z) {
   if (n == 0) return LFFN_OK;
   HashParams p{};
   p.x = d_x;
@@ -295,7 +333,7 @@ int launch_hash(lffn_ctx* c, const float* d_x, int64_t n, uint32_t* codes, float
     LFFN_CUDA(cudaGetLastError());
     return LFFN_OK;
   }
-  if (c->proj.kind == LFFN_PROJ_DENSE && !c->dense_exact && c->dense_ntile > 0) {
+  if (c->proj.kind == LFFN_PROJ_DENSE && !c->dense_exact && !exact_z && c->dense_ntile > 0) {
     // tcgen05 3xTF32 GEMM fused with codes / coefficients (dense_tcgen05.cuh)
     DenseParams d{};
     d.x = d_x;
@@ -441,26 +479,19 @@ int launch_gather_group(lffn_ctx* c, const uint32_t* codes, const float* coeff, 
   GatherParams p{};
   const size_t esz = c->t_dtype == LFFN_F32 ? 4 : 2;
   p.T = static_cast<const char*>(c->d_T) + size_t(k0) * size_t(c->rows) * size_t(c->cfg.d_out) * esz;
-  p.codes = codes + k0;
-  p.coeff = coeff + k0;
+  p.codes = codes + k0 * c->nc;
+  p.coeff = coeff + k0 * c->nc;
   p.y = y;
   p.n = n;
-  p.ld = int(c->h_loc);
-  p.nk = int(nk);
+  p.ld = int(c->h_loc * c->nc);
+  p.nk = int(nk * c->nc);
+  p.nc = int(c->nc);
   p.rows = int(c->rows);
   p.d_out = int(c->cfg.d_out);
   p.accumulate = accumulate;
   p.flag = c->d_flag;
   static const int rev = getenv("LFFN_GATHER_REVERSE") ? atoi(getenv("LFFN_GATHER_REVERSE")) : 0;
   p.reverse_odd_rounds = rev;
-  if (staged_gather_applicable(c->staged_ok, p, c->t_dtype)) {
-    int rc = launch_staged_gather(p, c->t_dtype, c->staged_smem, st);
-    ++c->launches;
-    if (rc == 0) {
-      LFFN_CUDA(cudaGetLastError());
-      return LFFN_OK;
-    }
-  }
   const bool f32 = c->t_dtype == LFFN_F32;
   const int vec = f32 ? ((p.d_out % 4 == 0) ? 4 : 1) : ((p.d_out % 8 == 0) ? 8 : 1);
   if (vec > 1) {
@@ -673,9 +704,9 @@ int lffn_ctx_create_shard(lffn_ctx** out, int device, int64_t max_tokens, const 
   // check_shapes (lookup.cpp:173-182)
   if (proj->d_in != cfg->d_in || proj->d_out != cfg->tables * cfg->code_bits)
     return fail(LFFN_ERR_USAGE, "lookup forward: projection must map d_in to h*tau");
-  if (cfg->neighbor_count != 1)
+  if (cfg->neighbor_count < 1 || cfg->neighbor_count > 256)
     return fail(LFFN_ERR_USAGE,
-                "lookup forward: the device path implements the top-1 default (neighbor_count 1)");
+                "lookup forward: the device path supports neighbor_count 1 .. 256");
   if (max_tokens < 0) return fail(LFFN_ERR_USAGE, "ctx_create: negative max_tokens");
   if (table_end == 0 && table_begin == 0) table_end = cfg->tables;
   if (table_begin < 0 || table_end > cfg->tables || table_begin > table_end)
@@ -707,6 +738,7 @@ int lffn_ctx_create_shard(lffn_ctx** out, int device, int64_t max_tokens, const 
   c->kb = table_begin;
   c->ke = table_end;
   c->h_loc = table_end - table_begin;
+  c->nc = cfg->neighbor_count;
 
   auto bail = [&](int rc) {
     destroy_ctx(c);
@@ -792,8 +824,10 @@ int lffn_ctx_create_shard(lffn_ctx** out, int device, int64_t max_tokens, const 
   }
 
   const size_t mt = size_t(std::max<int64_t>(max_tokens, 1));
-  CK(cudaMalloc(&c->d_codes, mt * size_t(std::max<int64_t>(c->h_loc, 1)) * sizeof(uint32_t)));
-  CK(cudaMalloc(&c->d_coeff, mt * size_t(std::max<int64_t>(c->h_loc, 1)) * sizeof(float)));
+  CK(cudaMalloc(&c->d_codes, mt * size_t(std::max<int64_t>(c->h_loc * c->nc, 1)) * sizeof(uint32_t)));
+  CK(cudaMalloc(&c->d_coeff, mt * size_t(std::max<int64_t>(c->h_loc * c->nc, 1)) * sizeof(float)));
+  if (c->nc > 1 && !c->d_zbuf)  // float64 z for the neighbour enumeration
+    CK(cudaMalloc(&c->d_zbuf, mt * size_t(c->code_width) * sizeof(double)));
   CK(cudaMalloc(&c->d_flag, sizeof(int)));
   CK(cudaMemset(c->d_flag, 0, sizeof(int)));
   CK(cudaMallocHost(&c->h_flag, sizeof(int)));
@@ -808,7 +842,6 @@ int lffn_ctx_create_shard(lffn_ctx** out, int device, int64_t max_tokens, const 
   CK(cudaEventCreate(&c->ev_t0));
   CK(cudaEventCreate(&c->ev_t1));
   CK(cudaEventCreate(&c->ev_t2));
-  c->staged_ok = staged_gather_configure(int(c->rows), int(cfg->d_out), &c->staged_smem);
   c->num_sms = prop.multiProcessorCount;
   if (const char* g = getenv("LFFN_TABLE_GROUP_MB")) c->table_group_bytes = size_t(atol(g)) << 20;
 #undef CK
@@ -928,7 +961,7 @@ int lffn_forward_host(lffn_ctx* c, const float* h_x, int64_t n, float* h_y) {
   const int64_t d_in = c->cfg.d_in, d_out = c->cfg.d_out;
   static const int want = getenv("LFFN_HOST_CHUNKS") ? atoi(getenv("LFFN_HOST_CHUNKS")) : 8;
   int nch = int(std::min<int64_t>(std::min(want, lffn_ctx::kChunks), std::max<int64_t>(1, n / 512)));
-  const bool dual = c->proj.kind != LFFN_PROJ_DENSE;
+  const bool dual = c->proj.kind != LFFN_PROJ_DENSE && c->nc == 1;
   const int64_t per = (n + nch - 1) / nch;
   for (int i = 0; i < nch; ++i) {
     const int64_t r0 = i * per, r1 = std::min(n, r0 + per);
@@ -938,10 +971,11 @@ int lffn_forward_host(lffn_ctx* c, const float* h_x, int64_t n, float* h_y) {
                               size_t(r1 - r0) * d_in * sizeof(float), cudaMemcpyHostToDevice, c->s_h2d));
     LFFN_CUDA(cudaEventRecord(c->ev_h2d[i], c->s_h2d));
     LFFN_CUDA(cudaStreamWaitEvent(sc, c->ev_h2d[i], 0));
-    if (int rc = launch_hash(c, c->d_xbuf + r0 * d_in, r1 - r0, c->d_codes + r0 * c->h_loc,
-                             c->d_coeff + r0 * c->h_loc, nullptr, sc))
+    const int64_t rec = r0 * c->h_loc * c->nc;
+    if (int rc = launch_hash(c, c->d_xbuf + r0 * d_in, r1 - r0, c->d_codes + rec, c->d_coeff + rec,
+                             nullptr, sc))
       return rc;
-    if (int rc = launch_gather(c, c->d_codes + r0 * c->h_loc, c->d_coeff + r0 * c->h_loc, r1 - r0,
+    if (int rc = launch_gather(c, c->d_codes + rec, c->d_coeff + rec, r1 - r0,
                                c->d_ybuf + r0 * d_out, 0, sc))
       return rc;
     LFFN_CUDA(cudaEventRecord(c->ev_comp[i], sc));

@@ -342,16 +342,20 @@ class LookupFFN:
         return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
 
     def hash(self, x, codes=None, coeff=None, z=None, stream=None):
-        """lffn_hash on device tensors; returns (codes, coeff[, z])."""
+        """lffn_hash on device tensors; returns (codes, coeff[, z]).  Shapes
+        [n, h_loc] for the top-1 default, [n, h_loc, nc] for neighbor_count nc
+        > 1 (the reference cache's slot order (i*h + k)*nc + c)."""
         import torch
 
         n = x.shape[0]
         hl = self.table_range[1] - self.table_range[0]
+        nc = self.cfg.neighbor_count
+        shape = (n, hl) if nc == 1 else (n, hl, nc)
         dev = x.device
         if codes is None:
-            codes = torch.empty((n, hl), dtype=torch.int32, device=dev)
+            codes = torch.empty(shape, dtype=torch.int32, device=dev)
         if coeff is None:
-            coeff = torch.empty((n, hl), dtype=torch.float32, device=dev)
+            coeff = torch.empty(shape, dtype=torch.float32, device=dev)
         zp = z.data_ptr() if z is not None else None
         check(_capi.lib().lffn_hash(self._ctx, x.data_ptr(), n, codes.data_ptr(), coeff.data_ptr(),
                                     zp, self._stream(stream)))

@@ -158,11 +158,11 @@ def test_device_path_fails_loudly_without_gpu():
         LookupFFN(cfg, proj, HashTables.init(cfg, 2), max_tokens=4)
 
 
-def test_nc_gt_1_is_rejected_not_emulated():
-    cfg = LookupConfig(d_in=8, d_out=4, tables=2, code_bits=3, neighbor_count=2)
-    proj = Projection.init(ProjectionSpec.signflip(8, 6), 1)
-    with pytest.raises(SizeError, match="top-1"):
-        LookupFFN(cfg, proj, HashTables.init(cfg, 2), max_tokens=4)
+def test_nc_above_device_limit_is_rejected_before_any_device_work():
+    cfg = LookupConfig(d_in=8, d_out=4, tables=2, code_bits=9, neighbor_count=257)
+    proj = Projection.init(ProjectionSpec.signflip(8, 18), 1)
+    with pytest.raises(SizeError, match="neighbor_count"):
+        LookupFFN(cfg, proj, None, max_tokens=4)
 
 
 def test_product_never_imports_the_oracle():
