@@ -9,7 +9,8 @@
 // flight per lane), gather_row_kernel (same without the 4-record layout) and
 // gather_direct_kernel (any width; NTOK tokens x one column chunk per warp).
 // Records are (table, neighbour) pairs, table-major: with neighbor_count nc
-// record r reads table r / nc (nc = 1 is the top-1 default).
+// record r reads table r / nc.  The row kernels serve nc = 1 (the top-1
+// default); nc > 1 takes gather_direct_kernel.
 #pragma once
 
 #include <cstdint>
@@ -168,7 +169,7 @@ __global__ void __launch_bounds__(256) gather_row_kernel(GatherParams p, int war
     for (int v = 0; v < VEC; ++v) acc[c][v] = 0.f;
 
   auto row_loads = [&](int k, uint32_t code, float (&vals)[MAXC][VEC]) {
-    const TT* rp = T + rec_table(p, k) * tstride + (int64_t)code * p.d_out + colbase;
+    const TT* rp = T + k * tstride + (int64_t)code * p.d_out + colbase;
 #pragma unroll
     for (int c = 0; c < MAXC; ++c) {
       if (c < nck && colbase + c * CHUNK < p.d_out) RowLoad<TT, VEC>::load(rp + c * CHUNK, vals[c]);
@@ -332,7 +333,7 @@ __global__ void __launch_bounds__(256, MINB) gather_row_persistent_kernel(Gather
         uint4 raw[TIF][MAXC];
 #pragma unroll
         for (int q = 0; q < TIF; ++q) {
-          const TT* rp = T + rec_table(p, kg + q0 + q) * tstride + (int64_t)codes4[q0 + q] * p.d_out + colbase;
+          const TT* rp = T + (kg + q0 + q) * tstride + (int64_t)codes4[q0 + q] * p.d_out + colbase;
 #pragma unroll
           for (int c = 0; c < MAXC; ++c)
             raw[q][c] = ok[c] ? Raw<TT>::load(rp + c * CHUNK) : make_uint4(0u, 0u, 0u, 0u);

@@ -186,7 +186,8 @@ __device__ __forceinline__ void phase_smem(double* sm, int t, int tpt, int lo, c
         v[r + 3] = (double)f.w;
       }
     } else {
-#pragma unroll 8
+      // fully unrolled: a dynamic index would move v[] to local memory
+#pragma unroll
       for (int r = 0; r < E; ++r) {
         const int a = t * E + r;
         double xv = 0.0;
@@ -256,16 +257,21 @@ __device__ __noinline__ double one_plus_exp_m2(double a) { return __dadd_rn(1.0,
 // K1 for structured projections (signflip, acdc) and the epilogue of the
 // dense projection (z_in given).
 // KIND: kPreSign (signflip), kPreDiag (acdc), kPreNone (dense epilogue on z_in).
-template <int LOGE, int KIND, int NT = 256, int MINB = 1>
+// LOGD > 0 fixes the transform width at compile time (with TR > 0 the
+// transform count): every phase's shared-memory geometry then folds into
+// constants, which removes most of the integer work around the butterflies.
+template <int LOGE, int KIND, int NT = 256, int MINB = 1, int LOGD = 0, int TR = 0>
 __global__ void __launch_bounds__(NT, MINB) hash_structured_kernel(HashParams p) {
   extern __shared__ double smem[];
   constexpr int E = 1 << LOGE;
-  const int tpt = p.threads_per_token;
+  const int logD = LOGD > 0 ? LOGD : p.logD;
+  const int ntr = TR > 0 ? TR : p.n_transforms;
+  const int tpt = LOGD > 0 ? (1 << (LOGD - LOGE)) : p.threads_per_token;
   const int slot = threadIdx.x / tpt;
   const int t = threadIdx.x - slot * tpt;
   const int64_t token = (int64_t)blockIdx.x * p.tokens_per_block + slot;
   const bool active = slot < p.tokens_per_block && token < p.n;
-  const int D = p.D;
+  const int D = 1 << logD;
   double* sm = smem + (size_t)slot * padded_len(D);
   int bad = 0;
 
@@ -284,15 +290,18 @@ __global__ void __launch_bounds__(NT, MINB) hash_structured_kernel(HashParams p)
   } else {
     const float* xr = p.x + token * (int64_t)p.d_in;
     int nph = 1;
-    if constexpr (LOGE > 0) nph = (p.logD + LOGE - 1) / LOGE;
-    for (int tr = 0; tr < p.n_transforms; ++tr) {
-      const bool last_tr = tr == p.n_transforms - 1;
+    if constexpr (LOGE > 0) nph = (logD + LOGE - 1) / LOGE;
+#pragma unroll 1
+    for (int tr = 0; tr < ntr; ++tr) {
+      const bool last_tr = tr == ntr - 1;
       if (active) run_first_phase<LOGE, KIND>(sm, t, tpt, p, tr, xr, bad, last_tr && nph == 1);
       token_sync();
-      for (int ph = 1; ph < nph; ++ph) {
+      const int nphc = LOGD > 0 ? (LOGD + LOGE - 1) / LOGE : nph;
+#pragma unroll
+      for (int ph = 1; ph < nphc; ++ph) {
         const int lo = ph * LOGE;
         if (active)
-          run_later_phase<LOGE>(sm, t, tpt, lo, min(LOGE, p.logD - lo), p, tr, bad,
+          run_later_phase<LOGE>(sm, t, tpt, lo, min(LOGE, logD - lo), p, tr, bad,
                                 last_tr && ph == nph - 1);
         token_sync();
       }
@@ -317,7 +326,37 @@ __global__ void __launch_bounds__(NT, MINB) hash_structured_kernel(HashParams p)
     const int hl = p.ke - p.kb;
     const int a_lo = t * E;
     const int a_hi = min(a_lo + E, p.code_width);
-    for (int k = max((a_lo + tau - 1) / tau, p.kb); k < p.ke && k * tau < a_hi; ++k) {
+    bool done = false;
+    if constexpr (E == 64 && KIND != kPreNone) {
+      if (!p.z_out && !p.scaled && p.code_width == D && (64 % tau) == 0) {
+        // tau | 64: the thread's 64 consecutive coordinates hold whole
+        // tables.  One 128-bit pass gives the sign bits and min |z|; when
+        // every |z| >= 18.5, each factor 1 + exp(-2|z|) rounds to exactly
+        // 1.0, so every weight is exactly 1 (lookup.cpp:185-189).
+        const double* q = sm + spos(a_lo);
+        uint64_t bits = 0;
+        double amin = 1e300;
+#pragma unroll
+        for (int r = 0; r < 64; r += 2) {
+          const double2 w2 = *reinterpret_cast<const double2*>(q + r);
+          bits |= uint64_t(w2.x >= 0.0 ? 1u : 0u) << r;
+          bits |= uint64_t(w2.y >= 0.0 ? 1u : 0u) << (r + 1);
+          amin = fmin(amin, fmin(fabs(w2.x), fabs(w2.y)));
+        }
+        if (amin >= 18.5) {
+          const uint32_t mask = (1u << tau) - 1u;
+          const int k0 = max(a_lo / tau, p.kb), k1 = min((a_lo + 64) / tau, p.ke);
+          uint32_t* cr = p.codes + token * hl - p.kb;
+          float* wr = p.coeff + token * hl - p.kb;
+          for (int k = k0; k < k1; ++k) {
+            cr[k] = uint32_t(bits >> (k * tau - a_lo)) & mask;
+            wr[k] = 1.0f;
+          }
+          done = true;
+        }
+      }
+    }
+    for (int k = max((a_lo + tau - 1) / tau, p.kb); !done && k < p.ke && k * tau < a_hi; ++k) {
       const int base = k * tau;
       uint32_t code = 0;
       bool small = false;

@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(128, 4) hash_pair_kernel(HashParams p) {
             v[r + 3] = (double)f.w;
           }
         } else {
-#pragma unroll 8
+#pragma unroll
           for (int r = 0; r < 32; ++r) {
             const int a = 32 * t + r;
             double xv = 0.0;

@@ -445,7 +445,11 @@ int launch_hash_top1(lffn_ctx* c, const float* d_x, int64_t n, uint32_t* codes, 
     return LFFN_OK;
   }
   if (nt == 128 && kind == kPreSign) {  // tuning variants (LFFN_HASH_VARIANT)
-    if (hvar == 1) go(hash_structured_kernel<6, kPreSign, 128, 3>);
+    // compile-time geometry for the BASELINE widths (D = 2048: c2, c3, c5;
+    // D = 4096: c4) and the signflip transform count
+    if (c->logD == 11 && c->n_transforms == 3) go(hash_structured_kernel<6, kPreSign, 128, 2, 11, 3>);
+    else if (c->logD == 12 && c->n_transforms == 3) go(hash_structured_kernel<6, kPreSign, 128, 2, 12, 3>);
+    else if (hvar == 1) go(hash_structured_kernel<6, kPreSign, 128, 3>);
     else if (hvar == 2) go(hash_structured_kernel<6, kPreSign, 128, 2>);
     else go(hash_structured_kernel<6, kPreSign, 128, 4>);
     ++c->launches;
@@ -494,7 +498,7 @@ int launch_gather_group(lffn_ctx* c, const uint32_t* codes, const float* coeff, 
   p.reverse_odd_rounds = rev;
   const bool f32 = c->t_dtype == LFFN_F32;
   const int vec = f32 ? ((p.d_out % 4 == 0) ? 4 : 1) : ((p.d_out % 8 == 0) ? 8 : 1);
-  if (vec > 1) {
+  if (vec > 1 && p.nc == 1) {
     // row-per-warp kernel: MAXC chunks of 32*vec columns per warp
     const int nchunks = (p.d_out + 32 * vec - 1) / (32 * vec);
     // chunks per warp: register budget of the persistent kernel (no spills)
