@@ -447,8 +447,8 @@ int launch_hash_top1(lffn_ctx* c, const float* d_x, int64_t n, uint32_t* codes, 
   if (nt == 128 && kind == kPreSign) {  // tuning variants (LFFN_HASH_VARIANT)
     // compile-time geometry for the BASELINE widths (D = 2048: c2, c3, c5;
     // D = 4096: c4) and the signflip transform count
-    if (c->logD == 11 && c->n_transforms == 3) go(hash_structured_kernel<6, kPreSign, 128, 2, 11, 3>);
-    else if (c->logD == 12 && c->n_transforms == 3) go(hash_structured_kernel<6, kPreSign, 128, 2, 12, 3>);
+    if (c->logD == 11 && c->n_transforms == 3) go(hash_structured_kernel<6, kPreSign, 128, 3, 11, 3>);
+    else if (c->logD == 12 && c->n_transforms == 3) go(hash_structured_kernel<6, kPreSign, 128, 3, 12, 3>);
     else if (hvar == 1) go(hash_structured_kernel<6, kPreSign, 128, 3>);
     else if (hvar == 2) go(hash_structured_kernel<6, kPreSign, 128, 2>);
     else go(hash_structured_kernel<6, kPreSign, 128, 4>);
