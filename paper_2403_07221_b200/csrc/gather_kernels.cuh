@@ -284,7 +284,7 @@ struct Raw {
 // (packed) while the (code, coeff) records of the next four tables are
 // prefetched.  Requires the 4-table record layout (nk % 4 == 0, ld % 4 == 0,
 // 16-byte aligned record pointers); 16-byte aligned rows (d_out % VEC == 0).
-template <typename TT, int MAXC, int TIF, int MINB>
+template <typename TT, int MAXC, int TIF, int MINB, bool PM = false>
 __global__ void __launch_bounds__(256, MINB) gather_row_persistent_kernel(GatherParams p,
                                                                           int warps_per_token) {
   constexpr int VEC = Raw<TT>::VEC;
@@ -297,8 +297,19 @@ __global__ void __launch_bounds__(256, MINB) gather_row_persistent_kernel(Gather
   const int64_t tstride = (int64_t)p.rows * p.d_out;
   int bad = 0;
   for (int64_t item = gwarp; item < p.n * warps_per_token; item += nwarps) {
-    const int64_t token = item / warps_per_token;
-    const int part = (int)(item - token * warps_per_token);
+    // part-major order: the resident warps work on one column part of many
+    // tokens, so a round of resident warps touches only that part of each
+    // table row -- HBM re-reads of an over-L2 table stack drop by the number
+    // of parts (c4: 4x), the gathered bytes are unchanged
+    int part;
+    int64_t token;
+    if constexpr (PM) {
+      part = (int)(item / p.n);
+      token = item - (int64_t)part * p.n;
+    } else {
+      token = item / warps_per_token;
+      part = (int)(item - token * warps_per_token);
+    }
     const int c0 = part * MAXC;
     const int colbase = c0 * CHUNK + lane * VEC;
     bool ok[MAXC];

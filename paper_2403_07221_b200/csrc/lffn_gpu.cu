@@ -516,6 +516,8 @@ int launch_gather_group(lffn_ctx* c, const uint32_t* codes, const float* coeff, 
       // persistent row kernel: grid = 2 CTAs per SM; 4 tables' packed rows
       // in flight per lane (the f32 6-chunk case keeps 4 x 6 x 16 B)
       const unsigned pg = (unsigned)std::min<int64_t>(int64_t(c->num_sms) * 2, (warps * 32 + 255) / 256);
+      // (MAXC 2 for bf16 -- 2x the column parts, half the bytes in flight per
+      // warp -- measured slower: c3 1.39 vs 1.22 ms, c4 2.47 vs 2.07 ms)
       const int pmaxc = f32 ? maxc : (nchunks <= 2 ? 2 : nchunks <= 3 ? 3 : 4);
       const int pwpt = (nchunks + pmaxc - 1) / pmaxc;
       const int64_t pwarps = n * pwpt;
@@ -524,7 +526,10 @@ int launch_gather_group(lffn_ctx* c, const uint32_t* codes, const float* coeff, 
       // (measured at c2 fp32: one warp per token with 6 chunks and 2 CTAs/SM
       // beats 2-3 warps per token at 3-4 CTAs/SM, 0.641 vs 0.698-0.942 ms;
       // L2 evict_last/evict_first splits of the table stack: 0.68-0.81 ms)
-#define LFFN_PROW(TT, M, TIF) gather_row_persistent_kernel<TT, M, TIF, 2><<<pgrid, 256, 0, st>>>(p, pwpt);
+      // several warps per token: part-major item order (gather_kernels.cuh)
+#define LFFN_PROW(TT, M, TIF)                                                      \
+  if (pwpt > 1) gather_row_persistent_kernel<TT, M, TIF, 2, true><<<pgrid, 256, 0, st>>>(p, pwpt); \
+  else gather_row_persistent_kernel<TT, M, TIF, 2, false><<<pgrid, 256, 0, st>>>(p, pwpt);
       if (f32) {
         if (pmaxc == 2) { LFFN_PROW(float, 2, 4) } else if (pmaxc == 4) { LFFN_PROW(float, 4, 4) }
         else { LFFN_PROW(float, 6, 4) }
