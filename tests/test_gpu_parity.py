@@ -66,6 +66,37 @@ def test_hash_bit_exact(oracle, shape, kind):
     np.testing.assert_allclose(coeff, w_ref.astype(np.float32), rtol=2.5e-7, atol=0)
 
 
+@pytest.mark.parametrize("shape", HASH_SHAPES + [(768, 768, 96, 10, 200), (1024, 1024, 100, 12, 64),
+                                   (2048, 2048, 100, 20, 40)],  # hash only: no tables built
+                         ids=lambda s: "x".join(map(str, s)))
+@pytest.mark.parametrize("kind", [ProjKind.signflip, ProjKind.acdc], ids=lambda k: k.name)
+def test_hash_codes_without_z(oracle, shape, kind):
+    """The production hash (no z copy-out; the vectorised epilogue for
+    tau | 64 with exact weight 1 when every |z| >= 18.5) against the oracle,
+    full stack and an odd table shard."""
+    d_in, d_out, h, tau, n = shape
+    kw = {"depth": 2} if kind == ProjKind.acdc else {}
+    cfg = LookupConfig(d_in=d_in, d_out=d_out, tables=h, code_bits=tau)
+    proj = Projection.init(ProjectionSpec(d_in, h * tau, kind, **kw), 1)
+    x = gaussian_matrix(n, d_in, 0).astype(np.float32)
+    layer = LookupFFN(cfg, proj, None, max_tokens=n)
+    codes, coeff, _ = device_hash(layer, x, want_z=False)
+    c, s = to_oracle(cfg, proj)
+    z_ref = oracle.proj_forward(s, proj.blob, x.astype(np.float64))
+    codes_ref, absz = oracle.compute_codes(z_ref, h, tau)
+    assert np.array_equal(codes, codes_ref)
+    w_ref = np.array([oracle.top1_weight(a) for a in absz.reshape(-1, tau)]).reshape(n, h)
+    np.testing.assert_allclose(coeff, w_ref.astype(np.float32), rtol=2.5e-7, atol=0)
+    if h < 3:
+        return
+    # a table shard with an odd start keeps the same codes
+    kb, ke = h // 3, h - 1
+    sh = LookupFFN(cfg, proj, None, max_tokens=n, table_range=(kb, ke))
+    codes_s, coeff_s, _ = device_hash(sh, x, want_z=False)
+    assert np.array_equal(codes_s, codes_ref[:, kb:ke])
+    np.testing.assert_allclose(coeff_s, coeff[:, kb:ke], rtol=0, atol=0)
+
+
 DENSE_SHAPES = [
     # d_in, d_out, h, tau, n
     (64, 64, 8, 4, 1000),       # c1
