@@ -27,7 +27,9 @@ struct BhParams {
   int stages;
 };
 
-template <int LOGE>
+// QPT: column quads per thread (D / 2048 for D >= 2048, else 1); every
+// thread owns 32 (token, column) outputs = QPT quads x (8 / QPT) tokens.
+template <int LOGE, int QPT>
 __global__ void __launch_bounds__(512, 1) hash_bh_kernel(HashParams p, BhParams bh) {
   extern __shared__ double smem[];
   constexpr int E = 1 << LOGE;
@@ -62,27 +64,86 @@ __global__ void __launch_bounds__(512, 1) hash_bh_kernel(HashParams p, BhParams 
   for (int s = 0; s < bh.stages; ++s) {
     // ---- block-diagonal multiply (projection.hpp:101-119)
     const double* Bs = bh.blocks + s * stage_size;
-    double acc[PAIRS];
+    if (b >= 4) {
+      // a thread's 4 consecutive columns (one quad) lie in one block g: per r
+      // it loads B_s[g][r][cc..cc+3] once (two 128-bit loads) and each token's
+      // src[g*b + r] once, and updates 4 x (8 / QPT) accumulators -- the
+      // reference's order (r ascending from 0.0), separate multiply and add
+      constexpr int TPQ = 8 / QPT;
+      const int nq = D >> 2;
+      int tok[TPQ];
+      int quad0, qstride;
+      if (nq >= NT) {
+        quad0 = tid;
+        qstride = NT;
 #pragma unroll
-    for (int j = 0; j < PAIRS; ++j) acc[j] = 0.0;
-    for (int r = 0; r < b; ++r) {
+        for (int j = 0; j < TPQ; ++j) tok[j] = j;
+      } else {
+        const int tpq = NT / nq;
+        quad0 = tid % nq;
+        qstride = 0;
+#pragma unroll
+        for (int j = 0; j < TPQ; ++j) tok[j] = tid / nq + tpq * j;
+      }
+      double acc[QPT][TPQ][4];
+#pragma unroll
+      for (int qi = 0; qi < QPT; ++qi) {
+        const int c = 4 * (quad0 + qi * qstride);
+        const int g = c >> logb, cc = c & (b - 1);
+        const double* Bp = Bs + ((size_t)g * b) * b + cc;
+        const int sb = spos(g << logb);
+#pragma unroll
+        for (int j = 0; j < TPQ; ++j)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[qi][j][v] = 0.0;
+        for (int r = 0; r < b; ++r) {
+          const double2 b01 = __ldg(reinterpret_cast<const double2*>(Bp + (size_t)r * b));
+          const double2 b23 = __ldg(reinterpret_cast<const double2*>(Bp + (size_t)r * b + 2));
+          const int so = sb + r + 2 * (r >> 6);  // spos(g*b + r): b | 64 or 64 | b
+#pragma unroll
+          for (int j = 0; j < TPQ; ++j) {
+            const double sv = smem[tok[j] * pad + so];
+            acc[qi][j][0] = __dadd_rn(acc[qi][j][0], __dmul_rn(sv, b01.x));
+            acc[qi][j][1] = __dadd_rn(acc[qi][j][1], __dmul_rn(sv, b01.y));
+            acc[qi][j][2] = __dadd_rn(acc[qi][j][2], __dmul_rn(sv, b23.x));
+            acc[qi][j][3] = __dadd_rn(acc[qi][j][3], __dmul_rn(sv, b23.y));
+          }
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int qi = 0; qi < QPT; ++qi) {
+        const int c = 4 * (quad0 + qi * qstride);
+#pragma unroll
+        for (int j = 0; j < TPQ; ++j)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) smem[tok[j] * pad + spos(c + v)] = acc[qi][j][v];
+      }
+      __syncthreads();
+    } else {
+      // b = 1, 2: one (token, column) per accumulator
+      double acc[PAIRS];
+#pragma unroll
+      for (int j = 0; j < PAIRS; ++j) acc[j] = 0.0;
+      for (int r = 0; r < b; ++r) {
+#pragma unroll
+        for (int j = 0; j < PAIRS; ++j) {
+          const int q = tid + NT * j;
+          const int t = q >> logD, c = q & (D - 1);
+          const int g = c >> logb, cc = c & (b - 1);
+          const double bv = __ldg(Bs + ((size_t)g * b + r) * b + cc);
+          const double sv = smem[t * pad + spos((g << logb) + r)];
+          acc[j] = __dadd_rn(acc[j], __dmul_rn(sv, bv));
+        }
+      }
+      __syncthreads();
 #pragma unroll
       for (int j = 0; j < PAIRS; ++j) {
         const int q = tid + NT * j;
-        const int t = q >> logD, c = q & (D - 1);
-        const int g = c >> logb, cc = c & (b - 1);
-        const double bv = __ldg(Bs + ((size_t)g * b + r) * b + cc);
-        const double sv = smem[t * pad + spos((g << logb) + r)];
-        acc[j] = __dadd_rn(acc[j], __dmul_rn(sv, bv));
+        smem[(q >> logD) * pad + spos(q & (D - 1))] = acc[j];
       }
+      __syncthreads();
     }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < PAIRS; ++j) {
-      const int q = tid + NT * j;
-      smem[(q >> logD) * pad + spos(q & (D - 1))] = acc[j];
-    }
-    __syncthreads();
     // ---- Hadamard transform of every token (fwht.hpp:28-41)
     const bool last_stage = s == bh.stages - 1;
     for (int ph = 0; ph < nph; ++ph) {

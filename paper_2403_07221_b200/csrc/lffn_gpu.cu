@@ -322,12 +322,18 @@ int launch_hash_top1(lffn_ctx* c, const float* d_x, int64_t n, uint32_t* codes, 
       kernel<<<grid, 512, smem, st>>>(p, bh);
     };
     switch (loge5) {
-      case 0: gob(hash_bh_kernel<0>); break;
-      case 1: gob(hash_bh_kernel<1>); break;
-      case 2: gob(hash_bh_kernel<2>); break;
-      case 3: gob(hash_bh_kernel<3>); break;
-      case 4: gob(hash_bh_kernel<4>); break;
-      default: gob(hash_bh_kernel<5>); break;
+      case 0: gob(hash_bh_kernel<0, 1>); break;
+      case 1: gob(hash_bh_kernel<1, 1>); break;
+      case 2: gob(hash_bh_kernel<2, 1>); break;
+      case 3: gob(hash_bh_kernel<3, 1>); break;
+      case 4: gob(hash_bh_kernel<4, 1>); break;
+      default:
+        // column quads per thread: D / 2048 for D >= 2048
+        if (c->D <= 2048) gob(hash_bh_kernel<5, 1>);
+        else if (c->D == 4096) gob(hash_bh_kernel<5, 2>);
+        else if (c->D == 8192) gob(hash_bh_kernel<5, 4>);
+        else gob(hash_bh_kernel<5, 8>);
+        break;
     }
     ++c->launches;
     LFFN_CUDA(cudaGetLastError());
