@@ -391,7 +391,8 @@ int launch_hash_top1(lffn_ctx* c, const float* d_x, int64_t n, uint32_t* codes, 
       return true;
     }();
     (void)fattr;
-    dense_fixup_kernel<<<unsigned(c->num_sms), 32 * kFixupWarps, fsm, st>>>(d);
+    // ~one entry per warp at c2 (2.7k entries): the serial float64 sums run in parallel
+    dense_fixup_kernel<<<unsigned(c->num_sms * 8), 32 * kFixupWarps, fsm, st>>>(d);
     ++c->launches;
     LFFN_CUDA(cudaGetLastError());
     return LFFN_OK;
