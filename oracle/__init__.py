@@ -146,6 +146,10 @@ class Oracle:
                                          C.c_void_p]
         L.orc_gather.argtypes = [_f64, C.c_size_t, C.c_size_t, C.c_size_t, _u32, _f64,
                                  C.c_size_t, _f64]
+        L.orc_proj_backward.argtypes = [C.POINTER(_SpecC), _f64, _f64, C.c_size_t, _f64, _f64,
+                                        _f64]
+        L.orc_lookup_backward.argtypes = [C.POINTER(_CfgC), C.POINTER(_SpecC), _f64, _f64, _f64,
+                                          C.c_size_t, _f64, _f64, _f64, _f64, C.c_void_p]
 
     # RNG -----------------------------------------------------------------
     def rng(self, seed: int):
@@ -251,6 +255,46 @@ class Oracle:
                             np.ascontiguousarray(coeff, np.float64), n, y)
         return y
 
+    @staticmethod
+    def param_count(s: Spec) -> int:
+        # Projection::param_count (projection.cpp:159-161): none for signflip
+        return 0 if s.kind == SIGNFLIP else s.blob_size()
+
+    def proj_backward(self, s: Spec, blob, x, grad_out):
+        """Projection::backward (projection.cpp:279-386) -> (grad_x, grad_params)."""
+        x = np.ascontiguousarray(x, np.float64)
+        go = np.ascontiguousarray(grad_out, np.float64)
+        n = x.shape[0]
+        gx = np.empty((n, s.d_in), np.float64)
+        gp = np.zeros(max(self.param_count(s), 1), np.float64)
+        rc = self.lib.orc_proj_backward(C.byref(_spec_c(s)), np.ascontiguousarray(blob, np.float64),
+                                        x, n, go, gx, gp)
+        if rc == 1:
+            raise ValueError("SizeError: projection backward")
+        if rc == 2:
+            raise ArithmeticError("NumericError: projection backward")
+        return gx, gp[:self.param_count(s)]
+
+    def lookup_backward(self, c: Cfg, s: Spec, blob, tables, x, grad_y):
+        """lookup_backward (lookup.cpp:292-347) -> dict(grad_x, grad_tables,
+        grad_proj, grad_z)."""
+        x = np.ascontiguousarray(x, np.float64)
+        gy = np.ascontiguousarray(grad_y, np.float64)
+        n = x.shape[0]
+        gx = np.empty((n, c.d_in), np.float64)
+        gt = np.zeros(c.tables * (1 << c.code_bits) * c.d_out, np.float64)
+        gp = np.zeros(max(self.param_count(s), 1), np.float64)
+        gz = np.empty((n, c.tables * c.code_bits), np.float64)
+        rc = self.lib.orc_lookup_backward(C.byref(_cfg_c(c)), C.byref(_spec_c(s)),
+                                          np.ascontiguousarray(blob, np.float64),
+                                          np.ascontiguousarray(tables, np.float64), x, n, gy, gx,
+                                          gt, gp, gz.ctypes.data)
+        if rc == 1:
+            raise ValueError("SizeError: lookup backward")
+        if rc == 2:
+            raise ArithmeticError("NumericError: lookup backward")
+        return dict(grad_x=gx, grad_tables=gt, grad_proj=gp[:self.param_count(s)], grad_z=gz)
+
 
 class Reference:
     """The reference library itself (oracle/_ref/liblffn_ref.so)."""
@@ -289,6 +333,11 @@ class Reference:
                                        [_f32, _f32, _f32, C.c_size_t, _f32, C.c_int, C.c_int,
                                         C.c_int])
         L.ref_pipeline_f32.restype = C.c_double
+        L.ref_lookup_backward.argtypes = ([C.c_int64] * 4 + [C.c_int, C.c_int64, C.c_int] +
+                                          [C.c_int64] * 3 + [_f64, C.c_int64, _f64, _f64,
+                                                             C.c_size_t, _f64, _f64, _f64, _f64])
+        L.ref_proj_backward.argtypes = ([C.c_int] + [C.c_int64] * 5 + [_f64, C.c_int64, _f64,
+                                                                     C.c_size_t, _f64, _f64, _f64])
         L.ref_bench_lookup_ffn.argtypes = ([C.c_int64] * 4 + [C.c_int, C.c_int] + [C.c_int64] * 3 +
                                            [C.c_size_t] * 3 + [C.c_int, C.c_int, C.c_uint64, _f64])
 
@@ -391,6 +440,37 @@ class Reference:
         if want_cache:
             return y, dict(z=z, codes=codes, weights=w, dots=dots)
         return y
+
+    def proj_backward(self, s: Spec, blob, x, grad_out):
+        x = np.ascontiguousarray(x, np.float64)
+        go = np.ascontiguousarray(grad_out, np.float64)
+        n = x.shape[0]
+        blob = np.ascontiguousarray(blob, np.float64)
+        gx = np.empty((n, s.d_in), np.float64)
+        pc = Oracle.param_count(s)
+        gp = np.zeros(max(pc, 1), np.float64)
+        rc = self.lib.ref_proj_backward(s.kind, s.d_in, s.d_out, s.stages, s.block, s.depth, blob,
+                                        blob.size, x, n, go, gx, gp)
+        if rc:
+            self._err(rc)
+        return gx, gp[:pc]
+
+    def lookup_backward(self, c: Cfg, s: Spec, blob, tables, x, grad_y):
+        x = np.ascontiguousarray(x, np.float64)
+        gy = np.ascontiguousarray(grad_y, np.float64)
+        n = x.shape[0]
+        blob = np.ascontiguousarray(blob, np.float64)
+        gx = np.empty((n, c.d_in), np.float64)
+        gt = np.zeros(c.tables * (1 << c.code_bits) * c.d_out, np.float64)
+        pc = Oracle.param_count(s)
+        gp = np.zeros(max(pc, 1), np.float64)
+        rc = self.lib.ref_lookup_backward(c.d_in, c.d_out, c.tables, c.code_bits, c.variant,
+                                          c.neighbor_count, s.kind, s.stages, s.block, s.depth,
+                                          blob, blob.size, np.ascontiguousarray(tables, np.float64),
+                                          x, n, gy, gx, gt, gp)
+        if rc:
+            self._err(rc)
+        return dict(grad_x=gx, grad_tables=gt, grad_proj=gp[:pc])
 
     def save_checkpoint(self, path: str, c: Cfg, s: Spec, blob, tables) -> None:
         blob = np.ascontiguousarray(blob, np.float64)

@@ -529,6 +529,195 @@ int orc_lookup_forward(const orc_cfg* c, const orc_proj_spec* ps, const double* 
   return bad ? 2 : 0;
 }
 
+/* block_diag_apply_transposed (projection.hpp:122-137) */
+static void orc_block_diag_apply_transposed(const double* in, double* out, const double* blocks,
+                                            size_t D, size_t b) {
+  const size_t groups = D / b;
+  for (size_t g = 0; g < groups; ++g) {
+    const double* blk = blocks + g * b * b;
+    const double* src = in + g * b;
+    double* dst = out + g * b;
+    for (size_t r = 0; r < b; ++r) {
+      double acc = 0.0;
+      const double* brow = blk + r * b;
+      for (size_t c = 0; c < b; ++c) acc += brow[c] * src[c];
+      dst[r] = acc;
+    }
+  }
+}
+
+/* Projection::backward (projection.cpp:279-386).  Rows are visited in order
+ * (the reference's gradient accumulation over rows is sequential). */
+int orc_proj_backward(const orc_proj_spec* s, const double* blob, const double* x, size_t n,
+                      const double* grad_out, double* grad_x, double* grad_params) {
+  if (orc_proj_validate(s)) return 1;
+  const size_t d_in = (size_t)s->d_in, d_out = (size_t)s->d_out;
+  if (!all_finite(grad_out, n * d_out)) return 2; /* "projection backward input" */
+  const size_t D = orc_transform_width(s);
+  if (s->kind == ORC_DENSE) {
+    for (size_t i = 0; i < n; ++i) {
+      const double* gi = grad_out + i * d_out;
+      const double* xi = x + i * d_in;
+      double* gxi = grad_x + i * d_in;
+      for (size_t k = 0; k < d_in; ++k) {
+        const double* wrow = blob + k * d_out;
+        double* gwrow = grad_params + k * d_out;
+        double acc = 0.0;
+        const double xv = xi[k];
+        for (size_t j = 0; j < d_out; ++j) {
+          acc += gi[j] * wrow[j];
+          gwrow[j] += xv * gi[j];
+        }
+        gxi[k] = acc;
+      }
+    }
+    return all_finite(grad_x, n * d_in) ? 0 : 2;
+  }
+  double* g = (double*)malloc(D * sizeof(double));
+  double* tmp = (double*)malloc(D * sizeof(double));
+  const size_t nst = s->kind == ORC_BH ? (size_t)s->stages : s->kind == ORC_ACDC ? 2 * (size_t)s->depth : 0;
+  double* stage_in = nst ? (double*)malloc(nst * D * sizeof(double)) : NULL;
+  for (size_t i = 0; i < n; ++i) {
+    if (nst) {
+      /* the forward's cached stage inputs for row i (projection.cpp:216-245) */
+      double* buf = g;
+      for (size_t j = 0; j < D; ++j) buf[j] = 0.0;
+      memcpy(buf, x + i * d_in, d_in * sizeof(double));
+      if (s->kind == ORC_BH) {
+        const size_t b = s->block == 0 ? D : (size_t)s->block;
+        const size_t stage_size = (D / b) * b * b;
+        for (size_t st = 0; st < nst; ++st) {
+          memcpy(stage_in + st * D, buf, D * sizeof(double));
+          orc_block_diag_apply(buf, tmp, blob + st * stage_size, D, b);
+          memcpy(buf, tmp, D * sizeof(double));
+          orc_fwht(buf, D);
+        }
+      } else {
+        for (size_t st = 0; st < (size_t)s->depth; ++st) {
+          const double* a = blob + 2 * st * D;
+          const double* d = a + D;
+          memcpy(stage_in + 2 * st * D, buf, D * sizeof(double));
+          for (size_t j = 0; j < D; ++j) buf[j] *= a[j];
+          orc_fwht(buf, D);
+          memcpy(stage_in + (2 * st + 1) * D, buf, D * sizeof(double));
+          for (size_t j = 0; j < D; ++j) buf[j] *= d[j];
+          orc_fwht(buf, D);
+        }
+      }
+    }
+    for (size_t j = 0; j < D; ++j) g[j] = 0.0;
+    memcpy(g, grad_out + i * d_out, d_out * sizeof(double));
+    if (s->kind == ORC_BH) {
+      const size_t b = s->block == 0 ? D : (size_t)s->block;
+      const size_t groups = D / b, stage_size = groups * b * b;
+      for (size_t st = (size_t)s->stages; st-- > 0;) {
+        orc_fwht(g, D);
+        const double* in = stage_in + st * D;
+        double* gblk = grad_params + st * stage_size;
+        for (size_t grp = 0; grp < groups; ++grp) {
+          const double* src = in + grp * b;
+          const double* gdst = g + grp * b;
+          double* gb = gblk + grp * b * b;
+          for (size_t r = 0; r < b; ++r) {
+            const double sv = src[r];
+            double* gbrow = gb + r * b;
+            for (size_t c = 0; c < b; ++c) gbrow[c] += sv * gdst[c];
+          }
+        }
+        orc_block_diag_apply_transposed(g, tmp, blob + st * stage_size, D, b);
+        memcpy(g, tmp, D * sizeof(double));
+      }
+    } else if (s->kind == ORC_ACDC) {
+      for (size_t st = (size_t)s->depth; st-- > 0;) {
+        const double* a = blob + 2 * st * D;
+        const double* d = a + D;
+        double* ga = grad_params + 2 * st * D;
+        double* gd = ga + D;
+        const double* pre_a = stage_in + 2 * st * D;
+        const double* pre_d = stage_in + (2 * st + 1) * D;
+        orc_fwht(g, D);
+        for (size_t j = 0; j < D; ++j) {
+          gd[j] += pre_d[j] * g[j];
+          g[j] *= d[j];
+        }
+        orc_fwht(g, D);
+        for (size_t j = 0; j < D; ++j) {
+          ga[j] += pre_a[j] * g[j];
+          g[j] *= a[j];
+        }
+      }
+    } else { /* signflip */
+      for (size_t st = 3; st-- > 0;) {
+        const double* sv = blob + st * D;
+        orc_fwht(g, D);
+        for (size_t j = 0; j < D; ++j) g[j] *= sv[j];
+      }
+    }
+    memcpy(grad_x + i * d_in, g, d_in * sizeof(double));
+  }
+  free(g);
+  free(tmp);
+  free(stage_in);
+  return all_finite(grad_x, n * d_in) ? 0 : 2; /* "projection backward output" */
+}
+
+/* lookup_backward (lookup.cpp:292-347) */
+int orc_lookup_backward(const orc_cfg* c, const orc_proj_spec* ps, const double* blob,
+                        const double* tables, const double* x, size_t n, const double* grad_y,
+                        double* grad_x, double* grad_tables, double* grad_params, double* grad_z) {
+  if (orc_cfg_validate(c)) return 1;
+  const size_t h = (size_t)c->tables, tau = (size_t)c->code_bits, nc = (size_t)c->neighbor_count;
+  const size_t d_out = (size_t)c->d_out, rows = (size_t)1 << tau, cw = h * tau;
+  const int scaled = (c->variant == ORC_SCALED || c->variant == ORC_GELU_TAU1);
+  if (!all_finite(grad_y, n * d_out)) return 2; /* "lookup backward input" */
+  double* y = (double*)malloc(sizeof(double) * (n * d_out + 1));
+  double* z = (double*)malloc(sizeof(double) * (n * cw + 1));
+  uint32_t* codes = (uint32_t*)malloc(sizeof(uint32_t) * (n * h * nc + 1));
+  double* w = (double*)malloc(sizeof(double) * (n * h * nc + 1));
+  double* dots = (double*)malloc(sizeof(double) * (n * h * nc + 1));
+  double* gz = grad_z ? grad_z : (double*)malloc(sizeof(double) * (n * cw + 1));
+  int rc = orc_lookup_forward(c, ps, blob, tables, x, n, y, z, codes, w, dots);
+  if (rc == 0) {
+    for (size_t q = 0; q < n * cw; ++q) gz[q] = 0.0;
+    for (size_t i = 0; i < n; ++i) {
+      const double* gy = grad_y + i * d_out;
+      for (size_t k = 0; k < h; ++k) {
+        const size_t ik = i * h + k;
+        const double* zk = z + ik * tau;
+        double* g = gz + i * cw + k * tau;
+        for (size_t cc = 0; cc < nc; ++cc) {
+          const size_t slot = ik * nc + cc;
+          const uint32_t code = codes[slot];
+          const double wt = w[slot], dot = dots[slot];
+          const double coeff = scaled ? wt * dot : wt;
+          const double* trow = tables + (k * rows + code) * d_out;
+          double* gtrow = grad_tables + (k * rows + code) * d_out;
+          double gdott = 0.0;
+          for (size_t j = 0; j < d_out; ++j) {
+            gdott += gy[j] * trow[j];
+            gtrow[j] += coeff * gy[j];
+          }
+          for (size_t j = 0; j < tau; ++j) {
+            const double sg = ((code >> j) & 1u) ? 1.0 : -1.0;
+            const double th = tanh(zk[j]);
+            const double dcoeff = scaled ? wt * (sg * (1.0 + dot) - dot * th) : wt * (sg - th);
+            g[j] += gdott * dcoeff;
+          }
+        }
+      }
+    }
+    rc = orc_proj_backward(ps, blob, x, n, gz, grad_x, grad_params);
+    if (rc == 0 && !all_finite(grad_tables, h * rows * d_out)) rc = 2; /* "lookup backward tables" */
+  }
+  free(y);
+  free(z);
+  free(codes);
+  free(w);
+  free(dots);
+  if (!grad_z) free(gz);
+  return rc;
+}
+
 void orc_gather(const double* tables, size_t h, size_t rows, size_t d_out, const uint32_t* codes,
                 const double* coeff, size_t n, double* y) {
 #pragma omp parallel for schedule(static)

@@ -87,6 +87,26 @@ int orc_lookup_forward(const orc_cfg* c, const orc_proj_spec* ps, const double* 
                        const double* tables, const double* x, size_t n, double* y, double* z_out,
                        uint32_t* codes_out, double* weights_out, double* dots_out);
 
+/*
+ * Projection::backward (projection.cpp:279-386): grad_x [n x d_in] and
+ * grad_params [param_count] (accumulated, caller zero-fills) from grad_out
+ * [n x d_out]; the bh / acdc stage inputs are recomputed from x as the
+ * forward cache holds them (projection.cpp:201-245).  0 ok, 1 usage, 2
+ * non-finite ("projection backward input/output").
+ */
+int orc_proj_backward(const orc_proj_spec* s, const double* blob, const double* x, size_t n,
+                      const double* grad_out, double* grad_x, double* grad_params);
+
+/*
+ * lookup_backward (lookup.cpp:292-347) at the forward's neighbour selection
+ * (recomputed from x): grad_tables [h][2^tau][d_out] and grad_params
+ * (accumulated, caller zero-fills), grad_x [n x d_in]; grad_z [n x h*tau]
+ * (optional) exposes the straight-through z gradient.
+ */
+int orc_lookup_backward(const orc_cfg* c, const orc_proj_spec* ps, const double* blob,
+                        const double* tables, const double* x, size_t n, const double* grad_y,
+                        double* grad_x, double* grad_tables, double* grad_params, double* grad_z);
+
 /* y = sum_k coeff[i,k] * T[k][code[i,k]] for precomputed codes/coeffs (the gather half) */
 void orc_gather(const double* tables, size_t h, size_t rows, size_t d_out, const uint32_t* codes,
                 const double* coeff, size_t n, double* y);

@@ -199,6 +199,58 @@ int ref_lookup_forward(int64_t d_in, int64_t d_out, int64_t h, int64_t tau, int 
   }
 }
 
+// lookup_forward with a cache, then lookup_backward (lookup.cpp:292-347):
+// grad_x [n x d_in], grad_tables [h][2^tau][d_out], grad_proj [param_count].
+int ref_lookup_backward(int64_t d_in, int64_t d_out, int64_t h, int64_t tau, int variant,
+                        int64_t nc, int kind, int64_t stages, int64_t block, int64_t depth,
+                        const double* blob, int64_t blob_len, const double* tables, const double* x,
+                        size_t n, const double* grad_y, double* grad_x, double* grad_tables,
+                        double* grad_proj) {
+  try {
+    LookupConfig cfg = make_cfg(d_in, d_out, h, tau, variant, nc);
+    ProjectionSpec s = make_spec(kind, d_in, h * tau, stages, block, depth);
+    Projection p = Projection::from_blob(s, std::vector<double>(blob, blob + blob_len));
+    HashTables t = HashTables::zeros_like(cfg);
+    std::memcpy(t.data.data(), tables, t.data.size() * sizeof(double));
+    DenseMatrix xm(n, size_t(d_in));
+    std::memcpy(xm.data.data(), x, n * size_t(d_in) * sizeof(double));
+    LookupCache cache;
+    lookup_forward(xm, p, t, cfg, &cache);
+    DenseMatrix gy(n, size_t(d_out));
+    std::memcpy(gy.data.data(), grad_y, n * size_t(d_out) * sizeof(double));
+    LookupGrads g = lookup_backward(gy, cache, p, t, cfg);
+    std::memcpy(grad_x, g.grad_x.data.data(), g.grad_x.data.size() * sizeof(double));
+    std::memcpy(grad_tables, g.grad_tables.data(), g.grad_tables.size() * sizeof(double));
+    std::memcpy(grad_proj, g.grad_proj.data(), g.grad_proj.size() * sizeof(double));
+    return 0;
+  } catch (const std::exception& e) {
+    return map_exc(e);
+  }
+}
+
+// Projection::backward (projection.cpp:279-386) with the forward's cache.
+int ref_proj_backward(int kind, int64_t d_in, int64_t d_out, int64_t stages, int64_t block,
+                      int64_t depth, const double* blob, int64_t blob_len, const double* x, size_t n,
+                      const double* grad_out, double* grad_x, double* grad_params) {
+  try {
+    ProjectionSpec s = make_spec(kind, d_in, d_out, stages, block, depth);
+    Projection p = Projection::from_blob(s, std::vector<double>(blob, blob + blob_len));
+    DenseMatrix xm(n, size_t(d_in));
+    std::memcpy(xm.data.data(), x, n * size_t(d_in) * sizeof(double));
+    ProjectionCache cache;
+    p.forward(xm, &cache);
+    DenseMatrix go(n, size_t(d_out));
+    std::memcpy(go.data.data(), grad_out, n * size_t(d_out) * sizeof(double));
+    std::vector<double> gp(p.param_count(), 0.0);
+    DenseMatrix gx = p.backward(go, xm, cache, gp);
+    std::memcpy(grad_x, gx.data.data(), gx.data.size() * sizeof(double));
+    std::memcpy(grad_params, gp.data(), gp.size() * sizeof(double));
+    return 0;
+  } catch (const std::exception& e) {
+    return map_exc(e);
+  }
+}
+
 // save_checkpoint / load_checkpoint (checkpoint.cpp:52-138).  load returns
 // the header fields in hdr[8] = {d_in, d_out, h, tau, variant, kind, m, b}
 // and copies blob / tables when the pointers are non-null.

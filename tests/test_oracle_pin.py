@@ -145,3 +145,31 @@ def test_non_finite_input(oracle, reference):
         oracle.lookup_forward(cfg, spec, blob, T, x)
     with pytest.raises(ArithmeticError, match="projection forward input"):
         reference.lookup_forward(cfg, spec, blob, T, x)
+
+
+@pytest.mark.parametrize("spec", SPECS, ids=lambda s: f"k{s.kind}-{s.d_in}x{s.d_out}-m{s.stages}b{s.block}d{s.depth}")
+def test_proj_backward(oracle, reference, spec):
+    """Projection::backward (projection.cpp:279-386): grad_x and the parameter
+    gradients, every kind (bh / acdc with the forward's stage inputs)."""
+    blob = reference.proj_init(spec, 7)
+    x = reference.gaussian(8, 9 * spec.d_in).reshape(9, spec.d_in)
+    go = reference.gaussian(9, 9 * spec.d_out).reshape(9, spec.d_out)
+    gx_o, gp_o = oracle.proj_backward(spec, blob, x, go)
+    gx_r, gp_r = reference.proj_backward(spec, blob, x, go)
+    assert bits_equal(gx_o, gx_r)
+    assert bits_equal(gp_o, gp_r)
+
+
+@pytest.mark.parametrize("case", FWD, ids=lambda c: f"{c[0].d_in}-{c[0].tables}x{c[0].code_bits}-v{c[0].variant}-nc{c[0].neighbor_count}-k{c[1]['kind']}")
+def test_lookup_backward(oracle, reference, case):
+    """lookup_backward (lookup.cpp:292-347): grad_tables, grad_proj, grad_x."""
+    cfg, kw = case
+    spec = cfg.spec(**kw)
+    blob = reference.proj_init(spec, 3)
+    T = reference.tables_init(cfg, 4)
+    x = reference.gaussian(5, 11 * cfg.d_in).reshape(11, cfg.d_in)
+    gy = reference.gaussian(6, 11 * cfg.d_out).reshape(11, cfg.d_out)
+    g_o = oracle.lookup_backward(cfg, spec, blob, T, x, gy)
+    g_r = reference.lookup_backward(cfg, spec, blob, T, x, gy)
+    for k in ("grad_x", "grad_tables", "grad_proj"):
+        assert bits_equal(g_o[k], g_r[k]), k
