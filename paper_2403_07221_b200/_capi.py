@@ -62,6 +62,8 @@ SIGNATURES = {
     "lffn_lookup_accumulate": (C.c_int, [_VP, _VP, _VP, _I64, _VP, C.c_int, _VP]),
     "lffn_forward": (C.c_int, [_VP, _VP, _I64, _VP, _VP]),
     "lffn_forward_host": (C.c_int, [_VP, _VP, _I64, _VP]),
+    "lffn_backward": (C.c_int, [_VP, _VP, _VP, _I64, _VP, _VP, _VP, _VP]),
+    "lffn_proj_backward": (C.c_int, [_VP, _VP, _VP, _I64, _VP, _VP, _VP]),
     "lffn_sync": (C.c_int, [_VP, _VP]),
     "lffn_ctx_set_option": (C.c_int, [_VP, C.c_int, _I64]),
     "lffn_ctx_launch_count": (_I64, [_VP]),

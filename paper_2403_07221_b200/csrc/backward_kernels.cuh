@@ -1,0 +1,376 @@
+// backward_kernels.cuh -- the LookupFFN backward on the device (SURVEY.md
+// 8f-4): lookup_backward (lookup.cpp:292-347) and Projection::backward
+// (projection.cpp:279-386) for the signflip and dense kinds.
+//
+//   KB1 bwd_gradz_kernel   per (token, table, neighbour) record: gdott =
+//                          <grad_y_i, T_k[code]> (fp32 products, float64
+//                          warp reduction), then the straight-through
+//                          gradient of every coordinate,
+//                          gz_j += gdott * w (s_j - tanh z_j)            (softmax)
+//                          gz_j += gdott * w (s_j (1 + dot) - dot tanh z_j)  (scaled)
+//                          with w, dot recomputed from z exactly as the
+//                          forward does (top-1 weight / exp(dot - logden)).
+//   KB2 grad_T             records bucketed per (table, code) row with
+//                          deterministic stable ranks (token blocks ranked
+//                          in order, block offsets, row starts by scan), then
+//                          one warp per row sums coeff * grad_y over its
+//                          records in the reference's order (tokens, then
+//                          neighbours ascending; float32) and writes the row
+//                          once -- no atomics on the gradient, run-to-run
+//                          identical.
+//   KB3 projection         signflip: the transposed network per token, in
+//                          float64 with the reference's stage order --
+//                          FWHT, x s_2, FWHT, x s_1, FWHT, x s_0 -- run as K1's
+//                          pre-flip phases with masks (0, s_2, s_1) and a final
+//                          flip by s_0: grad_x bit-identical to the reference
+//                          for the same grad_z.  dense: two exact float64
+//                          GEMMs, grad_x = g W^T (j ascending) and grad_W =
+//                          x^T g (tokens ascending), bit-identical as well.
+#pragma once
+
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "hash_kernels.cuh"
+#include "lffn_internal.h"
+
+namespace lffn_gpu {
+
+struct BwdParams {
+  const double* z;       // [n x code_width] forward projection output (float64)
+  const uint32_t* codes; // [n x hl x nc] records of the forward
+  const float* coeff;    // [n x hl x nc] forward coefficients
+  const float* gy;       // [n x d_out]
+  const void* T;         // this context's tables [hl][rows][d_out], f32 or bf16
+  int64_t n;
+  int d_out, code_width, tau, kb, hl, nc, rows, scaled;
+  double* gz;            // [n x code_width]: owned columns written, others untouched
+  uint32_t* offs;        // [hl * rows + 1] counts, then row starts
+  uint32_t* list;        // [n * hl * nc] record ids grouped by row
+  float* gT;             // [hl][rows][d_out]
+  int* flag;
+};
+
+template <typename TT>
+__device__ __forceinline__ float tload(const TT* p);
+template <>
+__device__ __forceinline__ float tload<float>(const float* p) { return __ldg(p); }
+template <>
+__device__ __forceinline__ float tload<__nv_bfloat16>(const __nv_bfloat16* p) {
+  return __bfloat162float(*p);
+}
+
+// KB1: one warp per token.  Lane j < tau owns coordinate j of the current
+// table; the sequential float64 reductions of the reference (sum |z|, the
+// top-1 divisions, log_denominator, code_dot) run on lane 0 over shuffled
+// coordinates, in the reference's order.
+template <typename TT, int VEC>
+__global__ void __launch_bounds__(256) bwd_gradz_kernel(BwdParams p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t token = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (token >= p.n) return;
+  const int tau = p.tau;
+  const float* gyr = p.gy + token * p.d_out;
+  const TT* T = static_cast<const TT*>(p.T);
+  int bad = 0;
+  for (int j = lane; j < p.d_out; j += 32)
+    if (!isfinite(gyr[j])) bad |= kFlagBwdInput;
+  for (int k = 0; k < p.hl; ++k) {
+    const double* zk = p.z + token * p.code_width + (int64_t)(p.kb + k) * tau;
+    const double zj = lane < tau ? zk[lane] : 0.0;
+    const double aj = fabs(zj);
+    // per-coordinate terms, then lane 0 folds them in order
+    const double fj = aj < 18.5 ? 1.0 + exp(-2.0 * aj) : 1.0;      // top-1 factor
+    const double lj = p.nc > 1 ? aj + log1p(exp(-2.0 * aj)) : 0.0;  // log_denominator term
+    double sum_abs = 0.0, w1 = 1.0, logden = 0.0;
+    for (int j = 0; j < tau; ++j) {
+      const double a = __shfl_sync(0xffffffffu, aj, j);
+      const double f = __shfl_sync(0xffffffffu, fj, j);
+      const double l = __shfl_sync(0xffffffffu, lj, j);
+      sum_abs = sum_abs + a;   // lookup.cpp:244-246
+      w1 = w1 / f;             // top1_weight (lookup.cpp:185-189)
+      logden = logden + l;     // lookup.cpp:102-109
+    }
+    double gzj = 0.0;
+    for (int c = 0; c < p.nc; ++c) {
+      const int64_t rec = (token * p.hl + k) * p.nc + c;
+      const uint32_t code = p.codes[rec];
+      const TT* row = T + ((int64_t)k * p.rows + code) * p.d_out;
+      float part = 0.f;
+      if constexpr (VEC == 4) {
+        for (int j = lane * 4; j < p.d_out; j += 128) {
+          const float4 g = *reinterpret_cast<const float4*>(gyr + j);
+          float t0, t1, t2, t3;
+          if constexpr (sizeof(TT) == 4) {
+            const float4 t = __ldg(reinterpret_cast<const float4*>(row + j));
+            t0 = t.x; t1 = t.y; t2 = t.z; t3 = t.w;
+          } else {
+            const uint2 u = __ldg(reinterpret_cast<const uint2*>(row + j));
+            t0 = __uint_as_float(u.x << 16); t1 = __uint_as_float(u.x & 0xffff0000u);
+            t2 = __uint_as_float(u.y << 16); t3 = __uint_as_float(u.y & 0xffff0000u);
+          }
+          part = fmaf(g.x, t0, part);
+          part = fmaf(g.y, t1, part);
+          part = fmaf(g.z, t2, part);
+          part = fmaf(g.w, t3, part);
+        }
+      } else {
+        for (int j = lane; j < p.d_out; j += 32) part = fmaf(gyr[j], tload<TT>(row + j), part);
+      }
+      double gd = (double)part;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) gd += __shfl_xor_sync(0xffffffffu, gd, o);
+      // the record's weight and dot exactly as the forward (lookup.cpp:238-252)
+      double dot = sum_abs, w = w1;
+      if (p.nc > 1) {
+        dot = 0.0;
+        for (int j = 0; j < tau; ++j) {
+          const double zz = __shfl_sync(0xffffffffu, zj, j);
+          dot = dot + (((code >> j) & 1u) ? zz : -zz);   // code_dot (lookup.cpp:111-116)
+        }
+        w = exp(dot - logden);
+      }
+      if (lane < tau) {
+        const double s = ((code >> lane) & 1u) ? 1.0 : -1.0;
+        const double th = tanh(zj);
+        const double dcoeff = p.scaled ? w * (s * (1.0 + dot) - dot * th) : w * (s - th);
+        gzj = gzj + gd * dcoeff;
+      }
+    }
+    if (lane < tau) p.gz[token * p.code_width + (int64_t)(p.kb + k) * tau + lane] = gzj;
+  }
+  if (bad) atomicOr(p.flag, bad);
+}
+
+// KB2a: deterministic ranks.  Thread (k, b) walks token block b in order
+// (tokens ascending, neighbours ascending) and gives each record of table k
+// its rank among the block's records of the same row; hist[k][b][code] ends
+// as the block's count.
+constexpr int kBwdBlocks = 32;  // token blocks of the rank pass
+__global__ void bwd_rank_kernel(BwdParams p, uint32_t* hist, uint32_t* rank) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= (int64_t)p.hl * kBwdBlocks) return;
+  const int k = int(tid % p.hl), b = int(tid / p.hl);
+  const int64_t per = (p.n + kBwdBlocks - 1) / kBwdBlocks;
+  const int64_t i0 = b * per, i1 = min(p.n, i0 + per);
+  uint32_t* h = hist + ((int64_t)k * kBwdBlocks + b) * p.rows;
+  for (int64_t i = i0; i < i1; ++i) {
+    const int64_t rec0 = (i * p.hl + k) * p.nc;
+    for (int c = 0; c < p.nc; ++c) {
+      const uint32_t code = p.codes[rec0 + c];
+      rank[rec0 + c] = h[code]++;
+    }
+  }
+}
+
+// KB2b': per (table, code): exclusive running sum of the block counts (the
+// block offsets, in place) and the row's total into offs.
+__global__ void bwd_block_offsets_kernel(BwdParams p, uint32_t* hist) {
+  const int64_t bin = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (bin >= (int64_t)p.hl * p.rows) return;
+  const int k = int(bin / p.rows), code = int(bin % p.rows);
+  uint32_t run = 0;
+  for (int b = 0; b < kBwdBlocks; ++b) {
+    uint32_t* hp = hist + ((int64_t)k * kBwdBlocks + b) * p.rows + code;
+    const uint32_t v = *hp;
+    *hp = run;
+    run += v;
+  }
+  p.offs[bin] = run;
+}
+
+// KB2b: exclusive scan of the row counts into row starts (one CTA).
+__global__ void __launch_bounds__(1024) bwd_scan_kernel(BwdParams p) {
+  __shared__ uint32_t warp_sums[32];
+  __shared__ uint32_t carry;
+  const int64_t bins = (int64_t)p.hl * p.rows;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < bins; base += blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    const uint32_t v = i < bins ? p.offs[i] : 0u;
+    // inclusive warp scan
+    uint32_t x = v;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      uint32_t s = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0u;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
+        if (lane >= o) s += y;
+      }
+      warp_sums[lane] = s;  // inclusive over warps
+    }
+    __syncthreads();
+    const uint32_t excl = carry + (wid > 0 ? warp_sums[wid - 1] : 0u) + x - v;
+    if (i < bins) p.offs[i] = excl;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) p.offs[bins] = carry;
+}
+
+// KB2c: record ids into their row's slots, stable (tokens ascending).
+__global__ void bwd_place_kernel(BwdParams p, const uint32_t* hist, const uint32_t* rank) {
+  const int64_t total = p.n * p.hl * p.nc;
+  const int64_t per = (p.n + kBwdBlocks - 1) / kBwdBlocks;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < total;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = r / ((int64_t)p.hl * p.nc);
+    const int k = int((r / p.nc) % p.hl);
+    const int b = int(i / per);
+    const uint32_t code = p.codes[r];
+    const uint32_t pos = p.offs[(int64_t)k * p.rows + code] +
+                         hist[((int64_t)k * kBwdBlocks + b) * p.rows + code] + rank[r];
+    p.list[pos] = uint32_t(r);
+  }
+}
+
+// KB2d: one warp per (table, code) row: gT_row = sum coeff * grad_y_token.
+__global__ void __launch_bounds__(256) bwd_gradT_kernel(BwdParams p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t bin = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t bins = (int64_t)p.hl * p.rows;
+  if (bin >= bins) return;
+  const uint32_t b0 = p.offs[bin], b1 = p.offs[bin + 1];
+  float* out = p.gT + bin * p.d_out;
+  const int per_tok = p.hl * p.nc;
+  int bad = 0;
+  for (int j0 = 0; j0 < p.d_out; j0 += 32 * 8) {
+    float acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = 0.f;
+    for (uint32_t e = b0; e < b1; ++e) {
+      const uint32_t rec = p.list[e];
+      const float cf = p.coeff[rec];
+      const float* gyr = p.gy + (int64_t)(rec / per_tok) * p.d_out;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int j = j0 + q * 32 + lane;
+        if (j < p.d_out) acc[q] = fmaf(cf, gyr[j], acc[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int j = j0 + q * 32 + lane;
+      if (j < p.d_out) {
+        if (!isfinite(acc[q])) bad |= kFlagBwdTables;
+        out[j] = acc[q];
+      }
+    }
+  }
+  if (bad) atomicOr(p.flag, bad);
+}
+
+// KB3 signflip: grad_x = first d_in of s_0 * H(s_1 * H(s_2 * H(g))), g = grad_z
+// padded to D (projection.cpp:362-369).  p.signmask holds (0, s_2, s_1).
+template <int LOGE>
+__global__ void __launch_bounds__(256) proj_bwd_signflip_kernel(HashParams p, const double* gz,
+                                                                const uint32_t* s0mask,
+                                                                double* grad_x) {
+  extern __shared__ double smem[];
+  constexpr int E = 1 << LOGE;
+  const int tpt = p.threads_per_token;
+  const int slot = threadIdx.x / tpt;
+  const int t = threadIdx.x - slot * tpt;
+  const int64_t token = (int64_t)blockIdx.x * p.tokens_per_block + slot;
+  const bool active = slot < p.tokens_per_block && token < p.n;
+  const int D = p.D;
+  double* sm = smem + (size_t)slot * padded_len(D);
+  int bad = 0;
+  auto token_sync = [&]() {
+    if (tpt <= 32) __syncwarp();
+    else asm volatile("bar.sync %0, %1;" ::"r"(slot + 1), "r"(tpt) : "memory");
+  };
+  if (active)
+    for (int a = t; a < D; a += tpt) {
+      const double v = a < p.code_width ? gz[token * p.code_width + a] : 0.0;
+      if (!isfinite(v)) bad |= kFlagBwdInput;
+      sm[spos(a)] = v;
+    }
+  token_sync();
+  int nph = 1;
+  if constexpr (LOGE > 0) nph = (p.logD + LOGE - 1) / LOGE;
+  for (int tr = 0; tr < 3; ++tr) {
+    if (active) phase_smem<LOGE, LOGE, false, kPreSign>(sm, t, tpt, 0, p, tr, nullptr, bad, false);
+    token_sync();
+    for (int ph = 1; ph < nph; ++ph) {
+      if (active) run_later_phase<LOGE>(sm, t, tpt, ph * LOGE, min(LOGE, p.logD - ph * LOGE), p, tr, bad, false);
+      token_sync();
+    }
+  }
+  if (active)
+    for (int a = t; a < p.d_in; a += tpt) {
+      double v = sm[spos(a)];
+      v = flip_sign(v, __ldg(s0mask + (a >> 5)), a & 31);
+      if (!isfinite(v)) bad |= kFlagBwdOutput;
+      grad_x[token * p.d_in + a] = v;
+    }
+  if (bad) atomicOr(p.flag, bad);
+}
+
+// KB3 dense: C[m][nn] = sum_kk A(m, kk) * B(kk, nn), kk ascending from 0.0 with
+// separately rounded multiply and add -- the reference's loops for grad_x
+// (j ascending) and grad_W (rows ascending).  64 x 64 tile per CTA, 4 x 4
+// outputs per thread, K staged through shared memory 16 at a time.
+template <typename TA, bool TRANS_A, bool TRANS_B>
+__global__ void __launch_bounds__(256) gemm_f64_exact_kernel(const TA* __restrict__ A, int lda,
+                                                             const double* __restrict__ B, int ldb,
+                                                             double* __restrict__ C, int ldc, int M,
+                                                             int N, int K, int* flag) {
+  __shared__ double As[16][65];
+  __shared__ double Bs[16][65];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    for (int q = threadIdx.x; q < 16 * 64; q += 256) {
+      const int kk = q / 64, mm = q % 64;
+      const int gm = m0 + mm, gk = k0 + kk;
+      double av = 0.0;
+      if (gm < M && gk < K) av = (double)(TRANS_A ? A[(int64_t)gk * lda + gm] : A[(int64_t)gm * lda + gk]);
+      As[kk][mm] = av;
+      const int gn = n0 + mm;
+      double bv = 0.0;
+      if (gn < N && gk < K) bv = TRANS_B ? B[(int64_t)gn * ldb + gk] : B[(int64_t)gk * ldb + gn];
+      Bs[kk][mm] = bv;
+    }
+    __syncthreads();
+    const int kmax = min(16, K - k0);
+    for (int kk = 0; kk < kmax; ++kk) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          acc[i][j] = __dadd_rn(acc[i][j], __dmul_rn(As[kk][ty * 4 + i], Bs[kk][tx * 4 + j]));
+    }
+    __syncthreads();
+  }
+  int bad = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gm = m0 + ty * 4 + i, gn = n0 + tx * 4 + j;
+      if (gm < M && gn < N) {
+        if (!isfinite(acc[i][j])) bad |= kFlagBwdOutput;
+        C[(int64_t)gm * ldc + gn] = acc[i][j];
+      }
+    }
+  if (bad && flag) atomicOr(flag, bad);
+}
+
+}  // namespace lffn_gpu

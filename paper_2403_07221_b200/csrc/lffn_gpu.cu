@@ -18,6 +18,7 @@
 #include "hash_kernels.cuh"
 #include "dense_tcgen05.cuh"
 #include "hash_bh_kernel.cuh"
+#include "backward_kernels.cuh"
 #include "hash_pair_kernel.cuh"
 #include "lffn_gpu.h"
 #include "lffn_internal.h"
@@ -73,6 +74,13 @@ struct lffn_ctx {
   long long* d_dense_prof = nullptr;  // LFFN_DENSE_PROF: per-CTA timestamps (debug)
   int64_t dense_prof_len = 0;
   double* d_zbuf = nullptr;  // dense: [max_tokens x code_width] float64
+  // backward scratch (allocated by the first lffn_backward / lffn_proj_backward)
+  double* d_gzbuf = nullptr;       // [max_tokens x code_width] float64 grad_z
+  uint32_t* d_bwd_offs = nullptr;  // [h_loc * rows + 1]
+  uint32_t* d_bwd_hist = nullptr;  // [h_loc * kBwdBlocks * rows]
+  uint32_t* d_bwd_rank = nullptr;  // [max_tokens * h_loc * nc]
+  uint32_t* d_bwd_list = nullptr;  // [max_tokens * h_loc * nc]
+  uint32_t* d_bwd_mask = nullptr;  // signflip: masks (0, s_2, s_1)
 
   // tables
   const void* d_T = nullptr;
@@ -104,6 +112,9 @@ int flag_message(int flag) {
   if (flag & kFlagInput) return fail(LFFN_ERR_NUMERIC, "non-finite values in projection forward input");
   if (flag & kFlagHash) return fail(LFFN_ERR_NUMERIC, "non-finite values in hash stage");
   if (flag & kFlagGather) return fail(LFFN_ERR_NUMERIC, "non-finite values in gather stage");
+  if (flag & kFlagBwdInput) return fail(LFFN_ERR_NUMERIC, "non-finite values in lookup backward input");
+  if (flag & kFlagBwdOutput) return fail(LFFN_ERR_NUMERIC, "non-finite values in projection backward output");
+  if (flag & kFlagBwdTables) return fail(LFFN_ERR_NUMERIC, "non-finite values in lookup backward tables");
   return LFFN_OK;
 }
 
@@ -153,6 +164,12 @@ void destroy_ctx(lffn_ctx* c) {
     cudaFree(c->d_dense_prof);
   }
   cudaFree(c->d_zbuf);
+  cudaFree(c->d_gzbuf);
+  cudaFree(c->d_bwd_offs);
+  cudaFree(c->d_bwd_hist);
+  cudaFree(c->d_bwd_rank);
+  cudaFree(c->d_bwd_list);
+  cudaFree(c->d_bwd_mask);
   cudaFree(c->d_T_owned);
   cudaFree(c->d_codes);
   cudaFree(c->d_coeff);
@@ -1003,6 +1020,185 @@ int lffn_forward_host(lffn_ctx* c, const float* h_x, int64_t n, float* h_y) {
                               size_t(r1 - r0) * d_out * sizeof(float), cudaMemcpyDeviceToHost, c->s_d2h));
   }
   return read_flag(c, c->s_d2h);
+}
+
+namespace lffn_gpu {
+
+// Backward scratch, allocated once per context on first use.
+int ensure_backward_scratch(lffn_ctx* c) {
+  const size_t mt = size_t(std::max<int64_t>(c->max_tokens, 1));
+  if (!c->d_zbuf) LFFN_CUDA(cudaMalloc(&c->d_zbuf, mt * size_t(c->code_width) * sizeof(double)));
+  if (!c->d_gzbuf) LFFN_CUDA(cudaMalloc(&c->d_gzbuf, mt * size_t(c->code_width) * sizeof(double)));
+  const size_t bins = size_t(std::max<int64_t>(c->h_loc, 1)) * size_t(c->rows);
+  if (!c->d_bwd_offs) {
+    LFFN_CUDA(cudaMalloc(&c->d_bwd_offs, (bins + 1) * sizeof(uint32_t)));
+    LFFN_CUDA(cudaMalloc(&c->d_bwd_hist, bins * kBwdBlocks * sizeof(uint32_t)));
+    LFFN_CUDA(cudaMalloc(&c->d_bwd_list, mt * size_t(std::max<int64_t>(c->h_loc * c->nc, 1)) * sizeof(uint32_t)));
+    LFFN_CUDA(cudaMalloc(&c->d_bwd_rank, mt * size_t(std::max<int64_t>(c->h_loc * c->nc, 1)) * sizeof(uint32_t)));
+  }
+  if (c->proj.kind == LFFN_PROJ_SIGNFLIP && !c->d_bwd_mask) {
+    const int64_t words = (c->D + 31) / 32;
+    LFFN_CUDA(cudaMalloc(&c->d_bwd_mask, size_t(3 * words) * sizeof(uint32_t)));
+    LFFN_CUDA(cudaMemset(c->d_bwd_mask, 0, size_t(words) * sizeof(uint32_t)));
+    LFFN_CUDA(cudaMemcpy(c->d_bwd_mask + words, c->d_signmask + 2 * words, size_t(words) * sizeof(uint32_t),
+                         cudaMemcpyDeviceToDevice));
+    LFFN_CUDA(cudaMemcpy(c->d_bwd_mask + 2 * words, c->d_signmask + words, size_t(words) * sizeof(uint32_t),
+                         cudaMemcpyDeviceToDevice));
+  }
+  return LFFN_OK;
+}
+
+// Projection::backward (projection.cpp:279-386) on device grad_z.
+int launch_proj_backward(lffn_ctx* c, const float* d_x, const double* gz, int64_t n, double* d_grad_x,
+                         double* d_grad_proj, cudaStream_t st) {
+  const int d_in = int(c->cfg.d_in), cw = int(c->code_width);
+  if (c->proj.kind == LFFN_PROJ_DENSE) {
+    if (d_grad_x) {
+      dim3 grid(unsigned((d_in + 63) / 64), unsigned((n + 63) / 64));
+      gemm_f64_exact_kernel<double, false, true><<<grid, 256, 0, st>>>(gz, cw, c->d_W, cw, d_grad_x, d_in,
+                                                                      int(n), d_in, cw, c->d_flag);
+      ++c->launches;
+    }
+    if (d_grad_proj) {
+      dim3 grid(unsigned((cw + 63) / 64), unsigned((d_in + 63) / 64));
+      gemm_f64_exact_kernel<float, true, false><<<grid, 256, 0, st>>>(d_x, d_in, gz, cw, d_grad_proj, cw,
+                                                                     d_in, cw, int(n), c->d_flag);
+      ++c->launches;
+    }
+    LFFN_CUDA(cudaGetLastError());
+    return LFFN_OK;
+  }
+  // signflip: grad_x only (the signs carry no gradient, param_count 0)
+  if (!d_grad_x) return LFFN_OK;
+  HashParams p{};
+  p.n = n;
+  p.d_in = d_in;
+  p.D = int(c->D);
+  p.logD = int(c->logD);
+  p.code_width = cw;
+  p.n_transforms = 3;
+  p.signmask = c->d_bwd_mask;
+  p.flag = c->d_flag;
+  const int loge = c->logD >= kMaxLogE ? kMaxLogE : int(c->logD);
+  const int tpt = int(c->D >> loge);
+  const int block = std::max(tpt, (256 / tpt) * tpt);
+  const int tpb = block / tpt;
+  p.tokens_per_block = tpb;
+  p.threads_per_token = tpt;
+  const size_t smem = size_t(tpb) * size_t(padded_len(int(c->D))) * sizeof(double);
+  const unsigned grid = unsigned((n + tpb - 1) / tpb);
+  auto go = [&](auto kernel) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    kernel<<<grid, block, smem, st>>>(p, gz, c->d_signmask, d_grad_x);
+  };
+  switch (loge) {
+    case 0: go(proj_bwd_signflip_kernel<0>); break;
+    case 1: go(proj_bwd_signflip_kernel<1>); break;
+    case 2: go(proj_bwd_signflip_kernel<2>); break;
+    case 3: go(proj_bwd_signflip_kernel<3>); break;
+    case 4: go(proj_bwd_signflip_kernel<4>); break;
+    case 5: go(proj_bwd_signflip_kernel<5>); break;
+    default: go(proj_bwd_signflip_kernel<6>); break;
+  }
+  ++c->launches;
+  LFFN_CUDA(cudaGetLastError());
+  return LFFN_OK;
+}
+
+int check_backward_kind(const lffn_ctx* c) {
+  if (c->proj.kind != LFFN_PROJ_SIGNFLIP && c->proj.kind != LFFN_PROJ_DENSE)
+    return fail(LFFN_ERR_USAGE, "backward: the device path implements the signflip and dense projections");
+  return LFFN_OK;
+}
+
+}  // namespace lffn_gpu
+
+int lffn_proj_backward(lffn_ctx* c, const float* d_x, const double* d_grad_z, int64_t n,
+                       double* d_grad_x, double* d_grad_proj, void* stream) {
+  if (!c) return fail(LFFN_ERR_USAGE, "null context");
+  if (int rc = check_n(c, n)) return rc;
+  if (int rc = check_backward_kind(c)) return rc;
+  if (n > 0 && (!d_x || !d_grad_z)) return fail(LFFN_ERR_USAGE, "projection backward: null buffer");
+  if (n == 0) return LFFN_OK;
+  DeviceGuard g(c->device);
+  if (int rc = ensure_backward_scratch(c)) return rc;
+  return launch_proj_backward(c, d_x, d_grad_z, n, d_grad_x, d_grad_proj,
+                              static_cast<cudaStream_t>(stream));
+}
+
+int lffn_backward(lffn_ctx* c, const float* d_x, const float* d_grad_y, int64_t n, double* d_grad_x,
+                  float* d_grad_tables, double* d_grad_proj, void* stream) {
+  if (!c) return fail(LFFN_ERR_USAGE, "null context");
+  if (int rc = check_n(c, n)) return rc;
+  if (int rc = check_backward_kind(c)) return rc;
+  if (n > 0 && (!d_x || !d_grad_y)) return fail(LFFN_ERR_USAGE, "lookup backward: null buffer");
+  if (!c->d_T) return fail(LFFN_ERR_USAGE, "lookup forward: tables not uploaded");
+  const int64_t bins = c->h_loc * c->rows;
+  if (n * c->h_loc * c->nc > int64_t(0xffffffffu) || bins > (int64_t(1) << 28))
+    return fail(LFFN_ERR_USAGE, "lookup backward: record or row count above the device limit");
+  DeviceGuard g(c->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (int rc = ensure_backward_scratch(c)) return rc;
+  const size_t esz = c->t_dtype == LFFN_F32 ? 4 : 2;
+  if (n > 0) {
+    // the forward's z (float64, exact), records and coefficients
+    if (c->nc == 1) {
+      if (int rc = launch_hash_top1(c, d_x, n, c->d_codes, c->d_coeff, c->d_zbuf, st, true)) return rc;
+    } else if (int rc = launch_hash(c, d_x, n, c->d_codes, c->d_coeff, c->d_zbuf, st)) {
+      return rc;
+    }
+    BwdParams p{};
+    p.z = c->d_zbuf;
+    p.codes = c->d_codes;
+    p.coeff = c->d_coeff;
+    p.gy = d_grad_y;
+    p.T = c->d_T;
+    p.n = n;
+    p.d_out = int(c->cfg.d_out);
+    p.code_width = int(c->code_width);
+    p.tau = int(c->cfg.code_bits);
+    p.kb = int(c->kb);
+    p.hl = int(c->h_loc);
+    p.nc = int(c->nc);
+    p.rows = int(c->rows);
+    p.scaled = (c->cfg.variant == LFFN_SCALED || c->cfg.variant == LFFN_GELU_TAU1) ? 1 : 0;
+    p.gz = c->d_gzbuf;
+    p.offs = c->d_bwd_offs;
+    p.list = c->d_bwd_list;
+    p.gT = d_grad_tables;
+    p.flag = c->d_flag;
+    LFFN_CUDA(cudaMemsetAsync(c->d_gzbuf, 0, size_t(n) * size_t(c->code_width) * sizeof(double), st));
+    if (c->h_loc > 0) {
+      const unsigned g1 = unsigned((n * 32 + 255) / 256);
+      const bool v4 = c->cfg.d_out % 4 == 0;
+      if (esz == 4 && v4) bwd_gradz_kernel<float, 4><<<g1, 256, 0, st>>>(p);
+      else if (esz == 4) bwd_gradz_kernel<float, 1><<<g1, 256, 0, st>>>(p);
+      else if (v4) bwd_gradz_kernel<__nv_bfloat16, 4><<<g1, 256, 0, st>>>(p);
+      else bwd_gradz_kernel<__nv_bfloat16, 1><<<g1, 256, 0, st>>>(p);
+      ++c->launches;
+    }
+    if (d_grad_tables && c->h_loc > 0) {
+      // deterministic buckets: ranks per token block, block offsets, row
+      // starts, stable placement, one warp per row
+      const int64_t hb = c->h_loc * kBwdBlocks;
+      LFFN_CUDA(cudaMemsetAsync(c->d_bwd_hist, 0, size_t(hb) * size_t(c->rows) * sizeof(uint32_t), st));
+      bwd_rank_kernel<<<unsigned((hb + 127) / 128), 128, 0, st>>>(p, c->d_bwd_hist, c->d_bwd_rank);
+      bwd_block_offsets_kernel<<<unsigned((bins + 255) / 256), 256, 0, st>>>(p, c->d_bwd_hist);
+      bwd_scan_kernel<<<1, 1024, 0, st>>>(p);
+      const unsigned gr = unsigned(std::min<int64_t>(int64_t(c->num_sms) * 8, (n * c->h_loc * c->nc + 255) / 256));
+      bwd_place_kernel<<<gr, 256, 0, st>>>(p, c->d_bwd_hist, c->d_bwd_rank);
+      bwd_gradT_kernel<<<unsigned((bins * 32 + 255) / 256), 256, 0, st>>>(p);
+      c->launches += 5;
+    }
+    LFFN_CUDA(cudaGetLastError());
+  } else if (d_grad_tables && c->h_loc > 0) {
+    LFFN_CUDA(cudaMemsetAsync(d_grad_tables, 0, size_t(bins) * size_t(c->cfg.d_out) * sizeof(float), st));
+  }
+  if (n > 0 && (d_grad_x || d_grad_proj))
+    return launch_proj_backward(c, d_x, c->d_gzbuf, n, d_grad_x, d_grad_proj, st);
+  if (n == 0 && d_grad_proj && c->proj.kind == LFFN_PROJ_DENSE)
+    LFFN_CUDA(cudaMemsetAsync(d_grad_proj, 0, size_t(c->cfg.d_in * c->code_width) * sizeof(double), st));
+  return LFFN_OK;
 }
 
 int lffn_sync(lffn_ctx* c, void* stream) {

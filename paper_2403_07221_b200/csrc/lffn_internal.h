@@ -29,6 +29,9 @@ enum : int {
   kFlagInput = 1,   // "projection forward input"
   kFlagHash = 2,    // "hash stage"
   kFlagGather = 4,  // "gather stage"
+  kFlagBwdInput = 8,    // "lookup backward input" / "projection backward input"
+  kFlagBwdOutput = 16,  // "projection backward output"
+  kFlagBwdTables = 32,  // "lookup backward tables"
 };
 
 }  // namespace lffn_gpu

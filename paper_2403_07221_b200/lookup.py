@@ -377,6 +377,48 @@ class LookupFFN:
                                        self._stream(stream)))
         return y
 
+    def backward(self, x, grad_y, want_x: bool = True, want_tables: bool = True,
+                 want_proj: bool = True, stream=None):
+        """lffn_backward (lookup_backward, lookup.cpp:292-347, + Projection::
+        backward) on device tensors: returns dict(grad_x [n, d_in] float64,
+        grad_tables [h_loc, 2^tau, d_out] float32, grad_proj float64 (dense:
+        [d_in, h*tau]; signflip: empty))."""
+        import torch
+
+        n = x.shape[0]
+        dev = x.device
+        cfg = self.cfg
+        hl = self.table_range[1] - self.table_range[0]
+        gx = torch.empty((n, cfg.d_in), dtype=torch.float64, device=dev) if want_x else None
+        gt = (torch.empty((hl, cfg.table_rows(), cfg.d_out), dtype=torch.float32, device=dev)
+              if want_tables else None)
+        dense = self.proj.spec.kind == ProjKind.dense if hasattr(self.proj, "spec") else \
+            self.proj.kind == ProjKind.dense
+        gp = (torch.empty((cfg.d_in, cfg.code_width()), dtype=torch.float64, device=dev)
+              if (want_proj and dense) else None)
+        ptr = (lambda t: t.data_ptr() if t is not None else None)
+        check(_capi.lib().lffn_backward(self._ctx, x.data_ptr(), grad_y.data_ptr(), n, ptr(gx),
+                                        ptr(gt), ptr(gp), self._stream(stream)))
+        return dict(grad_x=gx, grad_tables=gt,
+                    grad_proj=gp if gp is not None else torch.empty(0, dtype=torch.float64, device=dev))
+
+    def proj_backward(self, x, grad_z, stream=None):
+        """lffn_proj_backward (Projection::backward, projection.cpp:279-386)
+        for a float64 grad_z [n, h*tau]: (grad_x float64, grad_proj float64)."""
+        import torch
+
+        n = x.shape[0]
+        cfg = self.cfg
+        gx = torch.empty((n, cfg.d_in), dtype=torch.float64, device=x.device)
+        dense = self.proj.spec.kind == ProjKind.dense if hasattr(self.proj, "spec") else \
+            self.proj.kind == ProjKind.dense
+        gp = torch.empty((cfg.d_in, cfg.code_width()) if dense else (0,), dtype=torch.float64,
+                         device=x.device)
+        check(_capi.lib().lffn_proj_backward(self._ctx, x.data_ptr(), grad_z.data_ptr(), n,
+                                             gx.data_ptr(), gp.data_ptr() if dense else None,
+                                             self._stream(stream)))
+        return gx, gp
+
     def sync(self, stream=None) -> None:
         check(_capi.lib().lffn_sync(self._ctx, self._stream(stream)))
 
