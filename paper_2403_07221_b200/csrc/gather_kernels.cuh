@@ -326,25 +326,47 @@ __global__ void __launch_bounds__(256, MINB) gather_row_persistent_kernel(Gather
     // the tables a round finishes with (still in L2) are the first the next
     // round reads.
     const int rmask = (p.reverse_odd_rounds && ((item / nwarps) & 1)) ? -1 : 0;
-    auto group_of = [&](int it) { return rmask ? p.nk - 4 - it : it; };
-    uint4 cc = __ldg(reinterpret_cast<const uint4*>(cr + group_of(0)));
-    float4 ww = __ldg(reinterpret_cast<const float4*>(wr + group_of(0)));
-    for (int it = 0; it < p.nk; it += 4) {
-      const int kg = group_of(it);
-      uint4 cn = cc;
-      float4 wn = ww;
-      if (it + 4 < p.nk) {
-        cn = __ldg(reinterpret_cast<const uint4*>(cr + group_of(it + 4)));
-        wn = __ldg(reinterpret_cast<const float4*>(wr + group_of(it + 4)));
-      }
-      const uint32_t codes4[4] = {cc.x, cc.y, cc.z, cc.w};
-      const float w4[4] = {ww.x, ww.y, ww.z, ww.w};
+    // records in groups of G (= TIF, at least 4): G/4 128-bit loads each
+    constexpr int G = TIF > 4 ? TIF : 4;
+    auto group_of = [&](int it) { return rmask ? p.nk - G - it : it; };
+    uint4 cc[G / 4];
+    float4 ww[G / 4];
 #pragma unroll
-      for (int q0 = 0; q0 < 4; q0 += TIF) {
+    for (int g = 0; g < G / 4; ++g) {
+      cc[g] = __ldg(reinterpret_cast<const uint4*>(cr + group_of(0)) + g);
+      ww[g] = __ldg(reinterpret_cast<const float4*>(wr + group_of(0)) + g);
+    }
+    for (int it = 0; it < p.nk; it += G) {
+      const int kg = group_of(it);
+      uint4 cn[G / 4];
+      float4 wn[G / 4];
+#pragma unroll
+      for (int g = 0; g < G / 4; ++g) {
+        cn[g] = cc[g];
+        wn[g] = ww[g];
+      }
+      if (it + G < p.nk) {
+#pragma unroll
+        for (int g = 0; g < G / 4; ++g) {
+          cn[g] = __ldg(reinterpret_cast<const uint4*>(cr + group_of(it + G)) + g);
+          wn[g] = __ldg(reinterpret_cast<const float4*>(wr + group_of(it + G)) + g);
+        }
+      }
+      uint32_t codesG[G];
+      float wG[G];
+#pragma unroll
+      for (int g = 0; g < G / 4; ++g) {
+        codesG[4 * g] = cc[g].x; codesG[4 * g + 1] = cc[g].y;
+        codesG[4 * g + 2] = cc[g].z; codesG[4 * g + 3] = cc[g].w;
+        wG[4 * g] = ww[g].x; wG[4 * g + 1] = ww[g].y;
+        wG[4 * g + 2] = ww[g].z; wG[4 * g + 3] = ww[g].w;
+      }
+#pragma unroll
+      for (int q0 = 0; q0 < G; q0 += TIF) {
         uint4 raw[TIF][MAXC];
 #pragma unroll
         for (int q = 0; q < TIF; ++q) {
-          const TT* rp = T + (kg + q0 + q) * tstride + (int64_t)codes4[q0 + q] * p.d_out + colbase;
+          const TT* rp = T + (kg + q0 + q) * tstride + (int64_t)codesG[q0 + q] * p.d_out + colbase;
 #pragma unroll
           for (int c = 0; c < MAXC; ++c)
             raw[q][c] = ok[c] ? Raw<TT>::load(rp + c * CHUNK) : make_uint4(0u, 0u, 0u, 0u);
@@ -352,10 +374,13 @@ __global__ void __launch_bounds__(256, MINB) gather_row_persistent_kernel(Gather
 #pragma unroll
         for (int q = 0; q < TIF; ++q)
 #pragma unroll
-          for (int c = 0; c < MAXC; ++c) Raw<TT>::fma(acc[c], w4[q0 + q], raw[q][c]);
+          for (int c = 0; c < MAXC; ++c) Raw<TT>::fma(acc[c], wG[q0 + q], raw[q][c]);
       }
-      cc = cn;
-      ww = wn;
+#pragma unroll
+      for (int g = 0; g < G / 4; ++g) {
+        cc[g] = cn[g];
+        ww[g] = wn[g];
+      }
     }
     float* yr = p.y + token * p.d_out;
 #pragma unroll
