@@ -551,8 +551,8 @@ int launch_gather_group(lffn_ctx* c, const uint32_t* codes, const float* coeff, 
       // beats 2-3 warps per token at 3-4 CTAs/SM, 0.641 vs 0.698-0.942 ms;
       // L2 evict_last/evict_first splits of the table stack: 0.68-0.81 ms)
       // (c3 with 2 column parts and 8 tables in flight per lane measured
-      // 1.27 ms vs 1.22 ms: the bf16 gather is issue-bound -- 8 FFMA + 8
-      // unpack operations per 16-byte load -- rather than HBM-bound)
+      // 1.27 ms vs 1.22 ms; packed FFMA2 accumulation measured slower for
+      // bf16 -- c4 2.31 vs 2.07 ms, c2 bf16 0.407 vs 0.393 ms)
       // several warps per token: part-major item order (gather_kernels.cuh)
 #define LFFN_PROW(TT, M, TIF)                                                      \
   if (pwpt > 1) gather_row_persistent_kernel<TT, M, TIF, 2, true><<<pgrid, 256, 0, st>>>(p, pwpt); \
