@@ -8,8 +8,11 @@ A step is one full forward (hash + gather-accumulate) over the workload's
 batch, inputs already resident in HBM.  Default workload: BASELINE.json
 configs[1] (c2: d=768, h=256, tau=8, 16384 tokens, signflip projection, fp32
 tables).  N > 1 (torchrun, one rank per GPU) shards TOKENS with replicated
-tables (weak scaling: every rank runs the full per-GPU batch; no collective
-on the data path).  Times are CUDA events on the launching
+tables for c1/c2/c5 (weak scaling: every rank runs the full per-GPU batch; no
+collective on the data path) and TABLES for c3/c4 (strong
+scaling: every rank runs all tokens over its table slice; the fp32 partials
+are combined by NCCL reduce-scatter (c3) / all-reduce (c4), chunk-pipelined;
+--shard overrides).  Times are CUDA events on the launching
 stream, per step, with L2 flushed (256 MiB write) before every timed step;
 the max over ranks is reported.
 
@@ -48,7 +51,23 @@ def parse():
     ap.add_argument("--tokens", type=int, default=0, help="override the batch size")
     ap.add_argument("--cpu-sample", type=int, default=0, help="reference-arm tokens per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", default="auto", choices=["auto", "token", "table"],
+                    help="N>1 partitioning: token (tables replicated, c1/c2/c5) or table "
+                         "(tables split over ranks, partials combined by NCCL; c3/c4); "
+                         "auto picks the north star's choice per config")
     return ap.parse_args()
+
+
+def shard_mode(args) -> tuple:
+    """(mode, combine) per BASELINE north_star: c3 reduce-scatter, c4 all-reduce
+    over table shards at N > 1 (one GPU runs the plain forward; --shard table
+    forces the sharded path on a world-1 NCCL group); token sharding when the
+    tables fit one GPU."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.shard == "token" or (args.shard == "auto" and (args.config not in ("c3", "c4")
+                                                            or world == 1)):
+        return "token", None
+    return "table", ("all_reduce" if args.config == "c4" else "reduce_scatter")
 
 
 def dist_env():
@@ -228,19 +247,52 @@ def run_ours(args):
     n = args.tokens or w.n
     kind = ProjKind[args.kind]
     cfg, proj, T = make_params(w, kind)
-    x = make_x(w, n, seed=rank)  # token sharding: rank r owns its own batch
+    mode, combine = shard_mode(args)
     elem = 4 if w.table_dtype == "f32" else 2
-    layer = LookupFFN(cfg, proj, T, device=local, max_tokens=n, table_dtype=w.table_dtype)
+    stream = torch.cuda.current_stream()
+    if mode == "token":
+        x = make_x(w, n, seed=rank)  # token sharding: rank r owns its own batch
+        layer = LookupFFN(cfg, proj, T, device=local, max_tokens=n, table_dtype=w.table_dtype)
+        sharded = None
+    else:
+        # table sharding: every rank holds all n tokens and tables
+        # [r*h/P, (r+1)*h/P); partial sums combined by NCCL (sharded.py)
+        from paper_2403_07221_b200.sharded import ShardedLookupFFN
+
+        if dist is None:  # one GPU: a world-1 NCCL group keeps the same code path
+            import socket
+
+            import torch.distributed as dist
+
+            with socket.socket() as sk:
+                sk.bind(("127.0.0.1", 0))
+                port = sk.getsockname()[1]
+            dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0,
+                                    world_size=1, device_id=torch.device("cuda", local))
+
+        chunks = 4
+        q = world * chunks
+        n = ((n + q - 1) // q) * q
+        x = make_x(w, n, seed=0)
+        sharded = ShardedLookupFFN(cfg, proj, T, mode="table", combine=combine, device=local,
+                                   max_tokens=n, table_dtype=w.table_dtype, chunks=chunks)
+        layer = sharded.layer
     del T
 
-    stream = torch.cuda.current_stream()
     xd = torch.from_numpy(x).cuda()
     yd = torch.empty((n, cfg.d_out), dtype=torch.float32, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     layer.set_timing(True)
 
-    def step():
-        layer.forward_device(xd, yd, stream=stream)
+    if sharded is None:
+        def step():
+            layer.forward_device(xd, yd, stream=stream)
+    else:
+        y_sh = torch.empty((n // world if combine == "reduce_scatter" else n, cfg.d_out),
+                           dtype=torch.float32, device="cuda")
+
+        def step():
+            sharded.forward(xd, y_sh)
 
     for _ in range(args.warmup):
         flush.fill_(1)
@@ -261,10 +313,20 @@ def run_ours(args):
             evs[i][0].record(stream)
             step()
             evs[i][1].record(stream)
-            a, b = layer.stage_ms()        # event sync on this step's stage events
+            if sharded is None:
+                a, b = layer.stage_ms()    # event sync on this step's stage events
+                hash_ms.append(a)
+                gather_ms.append(b)
+        torch.cuda.synchronize()
+    if sharded is not None:
+        # the rank's kernels alone (hash + gather of its table slice over all
+        # n tokens), timed outside the sharded steps
+        for i in range(max(3, args.steps // 2)):
+            flush.fill_(i & 0xFF)
+            layer.forward_device(xd, yd, stream=stream)
+            a, b = layer.stage_ms()
             hash_ms.append(a)
             gather_ms.append(b)
-        torch.cuda.synchronize()
     launches = layer.launch_count() - launches0
     layer.sync(stream)
     step_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
@@ -281,7 +343,8 @@ def run_ours(args):
     layer.sync()
     codes_np = codes.cpu().numpy().view(np.uint32)
     U = unique_table_bytes(codes_np, cfg, elem)
-    G = gathered_bytes_per_token(cfg, elem) * n
+    h_loc = layer.table_range[1] - layer.table_range[0]
+    G = gathered_bytes_per_token(cfg, elem) * n * h_loc // cfg.tables  # this rank's tables
 
     # end-to-end through the C-ABI host path: pinned host x -> y
     hx = torch.from_numpy(x).pin_memory()
@@ -316,7 +379,9 @@ def run_ours(args):
         achieved = G / (gather_avg * 1e-3) / 1e9
         peak_eff = G / (t_roof_ms * 1e-3) / 1e9
         fl = lookup_flops(cfg, proj.spec)
-        tokens_total = n * world
+        # token sharding: every rank its own n tokens; table sharding: the
+        # ranks share the same n tokens (each for its table slice)
+        tokens_total = n * world if mode == "token" else n
         value = tokens_total / (mean_ms * 1e-3)
         traffic = load_traffic(args.config, args.kind)
         result = {
@@ -328,7 +393,7 @@ def run_ours(args):
             "warmup": args.warmup,
             "ms_per_step": round(mean_ms, 5),
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "weak" if mode == "token" else "strong",
             "vs_baseline": None,
             "dtype": "f32" if w.table_dtype == "f32" else "bf16-tables/f32-accum",
             "data": "synthetic (reference seeds: x make_rng(rank), proj init seed 1, "
@@ -337,7 +402,10 @@ def run_ours(args):
                 "workload": f"{w.name}: d_in=d_out={w.d} h={w.h} tau={w.tau} "
                             f"n={n}/GPU {args.kind} {w.table_dtype} tables",
                 "tokens_per_gpu": n,
-                "parallelism": f"token-sharded x{world} (tables replicated)",
+                "parallelism": (f"token-sharded x{world} (tables replicated)" if mode == "token"
+                                else f"table-sharded x{world} (tables [{layer.table_range[0]}, "
+                                     f"{layer.table_range[1]}) on rank 0; NCCL {combine} of the "
+                                     f"fp32 partials, 4 chunks overlapped)"),
                 "l2": "flushed before every timed step (256 MiB write outside the events)",
             },
             "e2e": {
@@ -377,7 +445,10 @@ def run_ours(args):
     if dist:
         dist.barrier()
         dist.destroy_process_group()
-    layer.close()
+    if sharded is not None:
+        sharded.close()
+    else:
+        layer.close()
     return result
 
 

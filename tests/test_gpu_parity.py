@@ -358,3 +358,32 @@ def test_full_size_c2_codes_and_output(oracle):
     y_ref = oracle.gather(T.data.astype(np.float32).astype(np.float64), w.h, 1 << w.tau, w.d,
                           codes_ref, coeff.astype(np.float64))
     assert_close(y, y_ref, FP32_TOL, "c2 full size")
+
+
+def test_table_sharded_world1_nccl_path(oracle):
+    """The bench's table-sharded path (sharded.py, NCCL reduce-scatter) on a
+    world-1 group: y equals the plain forward."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2403_07221_b200.sharded import ShardedLookupFFN
+
+    cfg, proj, T, x = _setup(64, 64, 12, 4, ProjKind.signflip, 64)
+    plain = device_forward(LookupFFN(cfg, proj, T, max_tokens=64), x)
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        for combine in ("reduce_scatter", "all_reduce"):
+            sh = ShardedLookupFFN(cfg, proj, T, mode="table", combine=combine, device=0,
+                                  max_tokens=64, chunks=4)
+            y = sh.forward(torch.from_numpy(x).cuda())
+            torch.cuda.synchronize()
+            np.testing.assert_array_equal(y.cpu().numpy(), plain)
+            sh.close()
+    finally:
+        dist.destroy_process_group()
