@@ -189,18 +189,18 @@ int lffn_forward_host(lffn_ctx* ctx, const float* h_x, int64_t n, float* h_y);
  * lookup_backward (lookup.cpp:292-347) at the forward's neighbour selection,
  * recomputed from x on the device: d_grad_y [n x d_out] float32 in;
  * d_grad_x [n x d_in] float64, d_grad_tables [h_local][2^tau][d_out] float32
- * (overwritten), d_grad_proj float64 (dense: [d_in x h*tau] W gradient,
- * overwritten; signflip: none -- Projection::param_count is 0) out; any output
- * may be NULL.  A table shard produces its tables' gradient and the partial
- * grad_x / grad_W over its tables (sum over shards = full).  The device path
- * implements the signflip and dense projections (status 1 otherwise).
+ * (overwritten), d_grad_proj float64 in the blob layout (param_count entries:
+ * dense W [d_in x h*tau], acdc diagonals, bh blocks; signflip: none --
+ * Projection::param_count is 0; overwritten) out; any output may be NULL.  A
+ * table shard produces its tables' gradient and the partial grad_x /
+ * grad_proj over its tables (sum over shards = full).
  * Non-finite grad_y / outputs raise status 2 at lffn_sync ("lookup backward
  * input", "projection backward output", "lookup backward tables"). */
 int lffn_backward(lffn_ctx* ctx, const float* d_x, const float* d_grad_y, int64_t n,
                   double* d_grad_x, float* d_grad_tables, double* d_grad_proj, void* stream);
 /* Projection::backward (projection.cpp:279-386) for a given float64 grad_z
- * [n x h*tau]: grad_x (and the dense W gradient) bit-identical to the
- * reference for the same grad_z. */
+ * [n x h*tau]: grad_x and the parameter gradient bit-identical to the
+ * reference for the same grad_z (every kind). */
 int lffn_proj_backward(lffn_ctx* ctx, const float* d_x, const double* d_grad_z, int64_t n,
                        double* d_grad_x, double* d_grad_proj, void* stream);
 

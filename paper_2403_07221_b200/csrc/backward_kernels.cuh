@@ -322,11 +322,17 @@ __global__ void __launch_bounds__(256) proj_bwd_signflip_kernel(HashParams p, co
 // separately rounded multiply and add -- the reference's loops for grad_x
 // (j ascending) and grad_W (rows ascending).  64 x 64 tile per CTA, 4 x 4
 // outputs per thread, K staged through shared memory 16 at a time.
+// blockIdx.z selects a batch entry: A, B, C advance by sA, sB, sC elements.
 template <typename TA, bool TRANS_A, bool TRANS_B>
 __global__ void __launch_bounds__(256) gemm_f64_exact_kernel(const TA* __restrict__ A, int lda,
                                                              const double* __restrict__ B, int ldb,
                                                              double* __restrict__ C, int ldc, int M,
-                                                             int N, int K, int* flag) {
+                                                             int N, int K, int* flag,
+                                                             int64_t sA = 0, int64_t sB = 0,
+                                                             int64_t sC = 0) {
+  A += blockIdx.z * sA;
+  B += blockIdx.z * sB;
+  C += blockIdx.z * sC;
   __shared__ double As[16][65];
   __shared__ double Bs[16][65];
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
@@ -371,6 +377,128 @@ __global__ void __launch_bounds__(256) gemm_f64_exact_kernel(const TA* __restric
       }
     }
   if (bad && flag) atomicOr(flag, bad);
+}
+
+// ---- stagewise kernels of the acdc / bh projection backward ----------------
+// The stage vectors of all tokens live in [n x D] float64 arrays; every
+// operation is the reference's, in its order (projection.cpp:216-245 forward,
+// 322-360 backward).
+
+// V[i][:] = pad(x_i) to D (projection.cpp:212-213)
+__global__ void rows_pad_kernel(const float* __restrict__ x, int64_t n, int d_in, int D,
+                                double* __restrict__ V) {
+  const int64_t total = n * D;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = q / D;
+    const int j = int(q - i * D);
+    V[q] = j < d_in ? (double)x[i * d_in + j] : 0.0;
+  }
+}
+
+// V[i][:] (or its first `cols`) from a [n x cols] float64 array, zero padded
+__global__ void rows_load_kernel(const double* __restrict__ src, int64_t n, int cols, int D,
+                                 double* __restrict__ V, int* flag) {
+  const int64_t total = n * D;
+  int bad = 0;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = q / D;
+    const int j = int(q - i * D);
+    const double v = j < cols ? src[i * cols + j] : 0.0;
+    if (!isfinite(v)) bad |= kFlagBwdInput;
+    V[q] = v;
+  }
+  if (bad) atomicOr(flag, bad);
+}
+
+// out[i][:cols] = V[i][:cols]
+__global__ void rows_store_kernel(const double* __restrict__ V, int64_t n, int cols, int D,
+                                  double* __restrict__ out, int* flag) {
+  const int64_t total = n * cols;
+  int bad = 0;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = q / cols;
+    const double v = V[i * D + (q - i * cols)];
+    if (!isfinite(v)) bad |= kFlagBwdOutput;
+    out[q] = v;
+  }
+  if (bad) atomicOr(flag, bad);
+}
+
+// V[i][j] *= diag[j]
+__global__ void rows_scale_kernel(double* __restrict__ V, int64_t n, int D,
+                                  const double* __restrict__ diag) {
+  const int64_t total = n * D;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total;
+       q += (int64_t)gridDim.x * blockDim.x)
+    V[q] = __dmul_rn(V[q], __ldg(diag + (q % D)));
+}
+
+// block_diag_apply (projection.hpp:101-119): out[g*b+c] = sum_r in[g*b+r] * B[g][r][c];
+// TRANS: block_diag_apply_transposed (:122-137): out[g*b+r] = sum_c B[g][r][c] * in[g*b+c]
+template <bool TRANS>
+__global__ void rows_blockdiag_kernel(const double* __restrict__ in, double* __restrict__ out,
+                                      int64_t n, int D, int b, const double* __restrict__ B) {
+  const int64_t total = n * D;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = q / D;
+    const int o = int(q - i * D);
+    const int g = o / b, t = o - g * b;
+    const double* src = in + i * D + (int64_t)g * b;
+    const double* blk = B + (int64_t)g * b * b;
+    double acc = 0.0;
+    if (TRANS) {
+      for (int c = 0; c < b; ++c) acc = __dadd_rn(acc, __dmul_rn(__ldg(blk + (int64_t)t * b + c), src[c]));
+    } else {
+      for (int r = 0; r < b; ++r) acc = __dadd_rn(acc, __dmul_rn(src[r], __ldg(blk + (int64_t)r * b + t)));
+    }
+    out[q] = acc;
+  }
+}
+
+// out[j] = sum_i A[i][j] * G[i][j], i ascending from 0.0 (the reference's
+// per-row accumulation of ga / gd, projection.cpp:345-356)
+__global__ void colsum_prod_kernel(const double* __restrict__ A, const double* __restrict__ G,
+                                   int64_t n, int D, double* __restrict__ out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= D) return;
+  double acc = 0.0;
+  for (int64_t i = 0; i < n; ++i) acc = __dadd_rn(acc, __dmul_rn(A[i * D + j], G[i * D + j]));
+  out[j] = acc;
+}
+
+// in-place FWHT of every row (fwht.hpp:28-41), K1's phases in shared memory
+template <int LOGE>
+__global__ void __launch_bounds__(256) rows_fwht_kernel(HashParams p, double* __restrict__ V) {
+  extern __shared__ double smem[];
+  const int tpt = p.threads_per_token;
+  const int slot = threadIdx.x / tpt;
+  const int t = threadIdx.x - slot * tpt;
+  const int64_t token = (int64_t)blockIdx.x * p.tokens_per_block + slot;
+  const bool active = slot < p.tokens_per_block && token < p.n;
+  const int D = p.D;
+  double* sm = smem + (size_t)slot * padded_len(D);
+  int bad = 0;
+  auto token_sync = [&]() {
+    if (tpt <= 32) __syncwarp();
+    else asm volatile("bar.sync %0, %1;" ::"r"(slot + 1), "r"(tpt) : "memory");
+  };
+  if (active)
+    for (int a = t; a < D; a += tpt) sm[spos(a)] = V[token * D + a];
+  token_sync();
+  int nph = 1;
+  if constexpr (LOGE > 0) nph = (p.logD + LOGE - 1) / LOGE;
+  if (active) phase_smem<LOGE, LOGE, false, kPreNone>(sm, t, tpt, 0, p, 0, nullptr, bad, false);
+  token_sync();
+  for (int ph = 1; ph < nph; ++ph) {
+    if (active) run_later_phase<LOGE>(sm, t, tpt, ph * LOGE, min(LOGE, p.logD - ph * LOGE), p, 0, bad, false);
+    token_sync();
+  }
+  if (active)
+    for (int a = t; a < D; a += tpt) V[token * D + a] = sm[spos(a)];
 }
 
 }  // namespace lffn_gpu

@@ -81,6 +81,7 @@ struct lffn_ctx {
   uint32_t* d_bwd_rank = nullptr;  // [max_tokens * h_loc * nc]
   uint32_t* d_bwd_list = nullptr;  // [max_tokens * h_loc * nc]
   uint32_t* d_bwd_mask = nullptr;  // signflip: masks (0, s_2, s_1)
+  double* d_bwd_rows = nullptr;    // acdc / bh: (2 + stage inputs) x [max_tokens x D]
 
   // tables
   const void* d_T = nullptr;
@@ -170,6 +171,7 @@ void destroy_ctx(lffn_ctx* c) {
   cudaFree(c->d_bwd_rank);
   cudaFree(c->d_bwd_list);
   cudaFree(c->d_bwd_mask);
+  cudaFree(c->d_bwd_rows);
   cudaFree(c->d_T_owned);
   cudaFree(c->d_codes);
   cudaFree(c->d_coeff);
@@ -1051,6 +1053,121 @@ int ensure_backward_scratch(lffn_ctx* c) {
   return LFFN_OK;
 }
 
+// In-place FWHT of n rows of a [n x D] float64 array.
+int launch_rows_fwht(lffn_ctx* c, double* V, int64_t n, cudaStream_t st) {
+  HashParams p{};
+  p.n = n;
+  p.D = int(c->D);
+  p.logD = int(c->logD);
+  p.flag = c->d_flag;
+  const int loge = c->logD >= kMaxLogE ? kMaxLogE : int(c->logD);
+  const int tpt = int(c->D >> loge);
+  const int block = std::max(tpt, (256 / tpt) * tpt);
+  const int tpb = block / tpt;
+  p.tokens_per_block = tpb;
+  p.threads_per_token = tpt;
+  const size_t smem = size_t(tpb) * size_t(padded_len(int(c->D))) * sizeof(double);
+  const unsigned grid = unsigned((n + tpb - 1) / tpb);
+  auto go = [&](auto kernel) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    kernel<<<grid, block, smem, st>>>(p, V);
+  };
+  switch (loge) {
+    case 0: go(rows_fwht_kernel<0>); break;
+    case 1: go(rows_fwht_kernel<1>); break;
+    case 2: go(rows_fwht_kernel<2>); break;
+    case 3: go(rows_fwht_kernel<3>); break;
+    case 4: go(rows_fwht_kernel<4>); break;
+    case 5: go(rows_fwht_kernel<5>); break;
+    default: go(rows_fwht_kernel<6>); break;
+  }
+  ++c->launches;
+  return LFFN_OK;
+}
+
+// acdc / bh projection backward, stage by stage over [n x D] float64 arrays
+// (projection.cpp:322-360): the forward's stage inputs are recomputed, then
+// the stages run backwards; parameter gradients sum over the tokens in order.
+int launch_proj_backward_stagewise(lffn_ctx* c, const float* d_x, const double* gz, int64_t n,
+                                   double* d_grad_x, double* d_grad_proj, cudaStream_t st) {
+  const int64_t D = c->D;
+  const bool acdc = c->proj.kind == LFFN_PROJ_ACDC;
+  const int nst = acdc ? int(2 * c->proj.depth) : int(c->proj.stages);
+  const size_t mt = size_t(std::max<int64_t>(c->max_tokens, 1));
+  const size_t rows = mt * size_t(D);
+  if (!c->d_bwd_rows) LFFN_CUDA(cudaMalloc(&c->d_bwd_rows, size_t(2 + nst) * rows * sizeof(double)));
+  double* V = c->d_bwd_rows;
+  double* G = V + rows;
+  double* S = G + rows;
+  const size_t bytes = size_t(n) * size_t(D) * sizeof(double);
+  const unsigned ge = unsigned(std::min<int64_t>(int64_t(c->num_sms) * 16, (n * D + 255) / 256));
+  const int b = int(c->proj.block == 0 ? D : c->proj.block);
+  const int64_t stage_size = (D / b) * b * b;
+  // forward: the stage inputs (projection.cpp:216-245)
+  rows_pad_kernel<<<ge, 256, 0, st>>>(d_x, n, int(c->cfg.d_in), int(D), V);
+  ++c->launches;
+  for (int s = 0; s < (acdc ? nst / 2 : nst); ++s) {
+    if (acdc) {
+      const double* a = c->d_diag + 2 * s * D;
+      LFFN_CUDA(cudaMemcpyAsync(S + size_t(2 * s) * rows, V, bytes, cudaMemcpyDeviceToDevice, st));
+      rows_scale_kernel<<<ge, 256, 0, st>>>(V, n, int(D), a);
+      if (int rc = launch_rows_fwht(c, V, n, st)) return rc;
+      LFFN_CUDA(cudaMemcpyAsync(S + size_t(2 * s + 1) * rows, V, bytes, cudaMemcpyDeviceToDevice, st));
+      rows_scale_kernel<<<ge, 256, 0, st>>>(V, n, int(D), a + D);
+      if (int rc = launch_rows_fwht(c, V, n, st)) return rc;
+      c->launches += 2;
+    } else {
+      LFFN_CUDA(cudaMemcpyAsync(S + size_t(s) * rows, V, bytes, cudaMemcpyDeviceToDevice, st));
+      rows_blockdiag_kernel<false><<<ge, 256, 0, st>>>(V, G, n, int(D), b, c->d_bh + s * stage_size);
+      std::swap(V, G);
+      if (int rc = launch_rows_fwht(c, V, n, st)) return rc;
+      ++c->launches;
+    }
+  }
+  // backward (projection.cpp:322-360)
+  rows_load_kernel<<<ge, 256, 0, st>>>(gz, n, int(c->code_width), int(D), G, c->d_flag);
+  ++c->launches;
+  for (int s = (acdc ? nst / 2 : nst) - 1; s >= 0; --s) {
+    if (acdc) {
+      const double* a = c->d_diag + 2 * s * D;
+      if (int rc = launch_rows_fwht(c, G, n, st)) return rc;
+      if (d_grad_proj) {
+        colsum_prod_kernel<<<unsigned((D + 127) / 128), 128, 0, st>>>(S + size_t(2 * s + 1) * rows, G, n, int(D),
+                                                                        d_grad_proj + (2 * s + 1) * D);
+        ++c->launches;
+      }
+      rows_scale_kernel<<<ge, 256, 0, st>>>(G, n, int(D), a + D);
+      if (int rc = launch_rows_fwht(c, G, n, st)) return rc;
+      if (d_grad_proj) {
+        colsum_prod_kernel<<<unsigned((D + 127) / 128), 128, 0, st>>>(S + size_t(2 * s) * rows, G, n, int(D),
+                                                                        d_grad_proj + 2 * s * D);
+        ++c->launches;
+      }
+      rows_scale_kernel<<<ge, 256, 0, st>>>(G, n, int(D), a);
+      c->launches += 2;
+    } else {
+      if (int rc = launch_rows_fwht(c, G, n, st)) return rc;
+      if (d_grad_proj) {
+        // grad_B_s[g][r][c] = sum_i src_i[g*b + r] * g_i[g*b + c], tokens ascending
+        dim3 grid(unsigned((b + 63) / 64), unsigned((b + 63) / 64), unsigned(D / b));
+        gemm_f64_exact_kernel<double, true, false><<<grid, 256, 0, st>>>(
+            S + size_t(s) * rows, int(D), G, int(D), d_grad_proj + s * stage_size, b, b, b, int(n),
+            c->d_flag, b, b, int64_t(b) * b);
+        ++c->launches;
+      }
+      rows_blockdiag_kernel<true><<<ge, 256, 0, st>>>(G, V, n, int(D), b, c->d_bh + s * stage_size);
+      std::swap(V, G);
+      ++c->launches;
+    }
+  }
+  if (d_grad_x) {
+    rows_store_kernel<<<ge, 256, 0, st>>>(G, n, int(c->cfg.d_in), int(D), d_grad_x, c->d_flag);
+    ++c->launches;
+  }
+  LFFN_CUDA(cudaGetLastError());
+  return LFFN_OK;
+}
+
 // Projection::backward (projection.cpp:279-386) on device grad_z.
 int launch_proj_backward(lffn_ctx* c, const float* d_x, const double* gz, int64_t n, double* d_grad_x,
                          double* d_grad_proj, cudaStream_t st) {
@@ -1071,6 +1188,8 @@ int launch_proj_backward(lffn_ctx* c, const float* d_x, const double* gz, int64_
     LFFN_CUDA(cudaGetLastError());
     return LFFN_OK;
   }
+  if (c->proj.kind == LFFN_PROJ_ACDC || c->proj.kind == LFFN_PROJ_BH)
+    return launch_proj_backward_stagewise(c, d_x, gz, n, d_grad_x, d_grad_proj, st);
   // signflip: grad_x only (the signs carry no gradient, param_count 0)
   if (!d_grad_x) return LFFN_OK;
   HashParams p{};
@@ -1108,11 +1227,7 @@ int launch_proj_backward(lffn_ctx* c, const float* d_x, const double* gz, int64_
   return LFFN_OK;
 }
 
-int check_backward_kind(const lffn_ctx* c) {
-  if (c->proj.kind != LFFN_PROJ_SIGNFLIP && c->proj.kind != LFFN_PROJ_DENSE)
-    return fail(LFFN_ERR_USAGE, "backward: the device path implements the signflip and dense projections");
-  return LFFN_OK;
-}
+int check_backward_kind(const lffn_ctx*) { return LFFN_OK; }  // every projection kind
 
 }  // namespace lffn_gpu
 
@@ -1199,8 +1314,8 @@ int lffn_backward(lffn_ctx* c, const float* d_x, const float* d_grad_y, int64_t 
   }
   if (n > 0 && (d_grad_x || d_grad_proj))
     return launch_proj_backward(c, d_x, c->d_gzbuf, n, d_grad_x, d_grad_proj, st);
-  if (n == 0 && d_grad_proj && c->proj.kind == LFFN_PROJ_DENSE)
-    LFFN_CUDA(cudaMemsetAsync(d_grad_proj, 0, size_t(c->cfg.d_in * c->code_width) * sizeof(double), st));
+  if (n == 0 && d_grad_proj && c->proj.kind != LFFN_PROJ_SIGNFLIP)
+    LFFN_CUDA(cudaMemsetAsync(d_grad_proj, 0, size_t(blob_size(&c->proj)) * sizeof(double), st));
   return LFFN_OK;
 }
 

@@ -381,8 +381,8 @@ class LookupFFN:
                  want_proj: bool = True, stream=None):
         """lffn_backward (lookup_backward, lookup.cpp:292-347, + Projection::
         backward) on device tensors: returns dict(grad_x [n, d_in] float64,
-        grad_tables [h_loc, 2^tau, d_out] float32, grad_proj float64 (dense:
-        [d_in, h*tau]; signflip: empty))."""
+        grad_tables [h_loc, 2^tau, d_out] float32, grad_proj float64 in the
+        blob layout (dense: [d_in, h*tau]; signflip: empty))."""
         import torch
 
         n = x.shape[0]
@@ -392,10 +392,7 @@ class LookupFFN:
         gx = torch.empty((n, cfg.d_in), dtype=torch.float64, device=dev) if want_x else None
         gt = (torch.empty((hl, cfg.table_rows(), cfg.d_out), dtype=torch.float32, device=dev)
               if want_tables else None)
-        dense = self.proj.spec.kind == ProjKind.dense if hasattr(self.proj, "spec") else \
-            self.proj.kind == ProjKind.dense
-        gp = (torch.empty((cfg.d_in, cfg.code_width()), dtype=torch.float64, device=dev)
-              if (want_proj and dense) else None)
+        gp = self._grad_proj_buffer(dev) if want_proj else None
         ptr = (lambda t: t.data_ptr() if t is not None else None)
         check(_capi.lib().lffn_backward(self._ctx, x.data_ptr(), grad_y.data_ptr(), n, ptr(gx),
                                         ptr(gt), ptr(gp), self._stream(stream)))
@@ -410,14 +407,23 @@ class LookupFFN:
         n = x.shape[0]
         cfg = self.cfg
         gx = torch.empty((n, cfg.d_in), dtype=torch.float64, device=x.device)
-        dense = self.proj.spec.kind == ProjKind.dense if hasattr(self.proj, "spec") else \
-            self.proj.kind == ProjKind.dense
-        gp = torch.empty((cfg.d_in, cfg.code_width()) if dense else (0,), dtype=torch.float64,
-                         device=x.device)
+        gp = self._grad_proj_buffer(x.device)
         check(_capi.lib().lffn_proj_backward(self._ctx, x.data_ptr(), grad_z.data_ptr(), n,
-                                             gx.data_ptr(), gp.data_ptr() if dense else None,
+                                             gx.data_ptr(), gp.data_ptr() if gp is not None else None,
                                              self._stream(stream)))
-        return gx, gp
+        return gx, (gp if gp is not None else torch.empty(0, dtype=torch.float64, device=x.device))
+
+    def _grad_proj_buffer(self, dev):
+        """Projection::param_count (projection.cpp:159-161) float64 entries in the
+        blob layout (dense [d_in, h*tau]); None for signflip."""
+        import torch
+
+        spec = self.proj.spec if hasattr(self.proj, "spec") else self.proj
+        if spec.kind == ProjKind.signflip:
+            return None
+        if spec.kind == ProjKind.dense:
+            return torch.empty((spec.d_in, spec.d_out), dtype=torch.float64, device=dev)
+        return torch.empty(spec.blob_size(), dtype=torch.float64, device=dev)
 
     def sync(self, stream=None) -> None:
         check(_capi.lib().lffn_sync(self._ctx, self._stream(stream)))
