@@ -552,7 +552,9 @@ int launch_gather_group(lffn_ctx* c, const uint32_t* codes, const float* coeff, 
       // (measured at c2 fp32: one warp per token with 6 chunks and 2 CTAs/SM
       // beats 2-3 warps per token at 3-4 CTAs/SM, 0.641 vs 0.698-0.942 ms;
       // L2 evict_last/evict_first splits of the table stack: 0.68-0.81 ms)
-      // (c3 with 2 column parts and 8 tables in flight per lane measured
+      // (c2 fp32 with 2 column parts of 3 chunks, part-major, 4 or 8 tables in
+      // flight: 0.676 / 0.701 ms vs 0.641 ms one warp per token;
+      // c3 with 2 column parts and 8 tables in flight per lane measured
       // 1.27 ms vs 1.22 ms; packed FFMA2 accumulation measured slower for
       // bf16 -- c4 2.31 vs 2.07 ms, c2 bf16 0.407 vs 0.393 ms)
       // several warps per token: part-major item order (gather_kernels.cuh)
