@@ -16,7 +16,10 @@ run c5 --config c5 --steps 20 --warmup 5 --no-cpu-baseline
 run c1 --config c1 --steps 20 --warmup 5 --no-cpu-baseline
 run c2_dense --kind dense --steps 20 --warmup 5 --no-cpu-baseline
 run c2_bh --kind bh --steps 20 --warmup 5 --no-cpu-baseline
+run c3_table --config c3 --shard table --steps 10 --warmup 3 --no-cpu-baseline
 run reference --impl reference --steps 3 --warmup 3
+for k in signflip dense acdc bh; do timeout 300 python tools/backward_time.py c2 $k >> $out/${tag}_backward.txt 2>&1; done
+tail -4 $out/${tag}_backward.txt
 # launch list of the default bench (cold, serialised: shares only)
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file $out/${tag}_launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $out/${tag}_ncu_launches.log 2>&1
