@@ -211,8 +211,10 @@ int lffn_sync(lffn_ctx* ctx, void* stream);
 /* Context options:
  *   LFFN_OPT_DENSE_EXACT       1 = dense projection in exact float64 (z
  *                              bit-identical to projection.cpp:178-198);
- *                              0 (default) = tcgen05 3xTF32 GEMM (codes exact
- *                              wherever |z| > ~1e-5, BASELINE criterion)
+ *                              0 (default) = tcgen05 split-precision GEMM (bf16
+ *                              x3 terms, tf32 hi/lo when d_in % 8 != 0) with
+ *                              exact float64 recomputation of |z| < 1e-4, so
+ *                              codes stay bit-exact
  *   LFFN_OPT_TABLE_GROUP_BYTES walk the tables in L2-sized groups of this many
  *                              bytes (0 = one pass, the default) */
 #define LFFN_OPT_DENSE_EXACT 1

@@ -60,14 +60,13 @@ struct lffn_ctx {
   double* d_diag = nullptr;
   double* d_W = nullptr;
   double* d_bh = nullptr;   // bh: m x (D/b) x b x b blocks (float64)
-  float* d_wt_hi = nullptr;  // dense (tcgen05): slice of W^T, tf32 hi / lo split
-  float* d_wt_lo = nullptr;
+  void* d_wp[3] = {nullptr, nullptr, nullptr};  // dense (tcgen05): W^T slice split planes
   double* d_wt64 = nullptr;  // dense: slice of W^T in float64 (exact near-zero fixups)
   int dense_ntile = 0;       // N tile of the tcgen05 dense GEMM (0: exact path only)
   int dense_exact = 0;       // 1: exact float64 dense projection
-  alignas(64) CUtensorMap map_whi{}, map_wlo{}, map_xhi{}, map_xlo{};  // TMA maps (dense)
-  float* d_xhi = nullptr;  // dense: per-call tf32 hi / lo split of x (max_tokens x d_in)
-  float* d_xlo = nullptr;
+  alignas(64) DenseMaps dense_maps{};  // TMA maps of the split planes (dense)
+  void* d_xp[3] = {nullptr, nullptr, nullptr};  // dense: per-call split of x (max_tokens x d_in)
+  int dense_split = kSplitTf32;  // kSplitTf32 | kSplitBf16x3 (LFFN_DENSE_SPLIT=bf16x3)
   uint2* d_fix_list = nullptr;  // dense tcgen05: deferred exact fixups
   int* d_fix_count = nullptr;
   int fix_cap = 0;
@@ -147,11 +146,9 @@ void destroy_ctx(lffn_ctx* c) {
   cudaFree(c->d_diag);
   cudaFree(c->d_W);
   cudaFree(c->d_bh);
-  cudaFree(c->d_wt_hi);
-  cudaFree(c->d_wt_lo);
+  for (int q = 0; q < 3; ++q) cudaFree(c->d_wp[q]);
   cudaFree(c->d_wt64);
-  cudaFree(c->d_xhi);
-  cudaFree(c->d_xlo);
+  for (int q = 0; q < 3; ++q) cudaFree(c->d_xp[q]);
   cudaFree(c->d_fix_list);
   cudaFree(c->d_fix_count);
   if (c->d_dense_prof) {
@@ -197,25 +194,28 @@ void destroy_ctx(lffn_ctx* c) {
 // box_inner x box_outer, zero fill out of bounds.
 // tau values whose lcm(tau, 16) <= 128 (the tcgen05 path's N tile holds whole tables)
 template <int TAU>
-void launch_dense_tau(dim3 grid, size_t smem, cudaStream_t st, const CUtensorMap& a,
-                      const CUtensorMap& b, const CUtensorMap& c, const CUtensorMap& d,
+void launch_dense_tau(int split, dim3 grid, size_t smem, cudaStream_t st, const DenseMaps& m,
                       const DenseParams& p) {
   static bool attr = [&] {
-    cudaFuncSetAttribute(dense_tcgen05_kernel<TAU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(dense_smem_bytes(128)));
+    cudaFuncSetAttribute(dense_tcgen05_kernel<TAU, kSplitTf32>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(dense_smem_bytes(128, kSplitTf32)));
+    cudaFuncSetAttribute(dense_tcgen05_kernel<TAU, kSplitBf16x3>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(dense_smem_bytes(128, kSplitBf16x3)));
     return true;
   }();
   (void)attr;
-  dense_tcgen05_kernel<TAU><<<grid, 128, smem, st>>>(a, b, c, d, p);
+  if (split == kSplitBf16x3) dense_tcgen05_kernel<TAU, kSplitBf16x3><<<grid, 128, smem, st>>>(m, p);
+  else dense_tcgen05_kernel<TAU, kSplitTf32><<<grid, 128, smem, st>>>(m, p);
 }
 
-int launch_dense_tcgen05(int tau, dim3 grid, size_t smem, cudaStream_t st, const CUtensorMap& a,
-                         const CUtensorMap& b, const CUtensorMap& c, const CUtensorMap& d,
-                         const DenseParams& p) {
+int launch_dense_tcgen05(int tau, int split, dim3 grid, size_t smem, cudaStream_t st,
+                         const DenseMaps& m, const DenseParams& p) {
   switch (tau) {
 #define LFFN_TAU(T) \
   case T:           \
-    launch_dense_tau<T>(grid, smem, st, a, b, c, d, p); \
+    launch_dense_tau<T>(split, grid, smem, st, m, p); \
     return LFFN_OK;
     LFFN_TAU(1) LFFN_TAU(2) LFFN_TAU(3) LFFN_TAU(4) LFFN_TAU(5) LFFN_TAU(6) LFFN_TAU(7)
     LFFN_TAU(8) LFFN_TAU(10) LFFN_TAU(12) LFFN_TAU(14) LFFN_TAU(16) LFFN_TAU(20) LFFN_TAU(24)
@@ -225,8 +225,8 @@ int launch_dense_tcgen05(int tau, dim3 grid, size_t smem, cudaStream_t st, const
   }
 }
 
-int make_tma_map(CUtensorMap* map, const float* base, uint64_t inner, uint64_t outer,
-                 uint32_t box_inner, uint32_t box_outer) {
+int make_tma_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                 uint32_t box_inner, uint32_t box_outer, bool bf16 = false) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -237,14 +237,17 @@ int make_tma_map(CUtensorMap* map, const float* base, uint64_t inner, uint64_t o
     return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }();
   if (!encode) return fail(LFFN_ERR_RUNTIME, "cuTensorMapEncodeTiled unavailable");
+  const size_t eb = bf16 ? 2 : 4;
   const cuuint64_t dims[2] = {inner, std::max<uint64_t>(outer, 1)};
-  const cuuint64_t strides[1] = {inner * sizeof(float)};
+  const cuuint64_t strides[1] = {inner * eb};
   const cuuint32_t box[2] = {box_inner, box_outer};
   const cuuint32_t estr[2] = {1, 1};
-  const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
-                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                            box_inner * sizeof(float) == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
-                                                            : CU_TENSOR_MAP_SWIZZLE_128B,
+  const CUresult r = encode(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                            2, const_cast<void*>(base), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            box_inner * eb == 64   ? CU_TENSOR_MAP_SWIZZLE_64B
+                            : box_inner * eb == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                   : CU_TENSOR_MAP_SWIZZLE_128B,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
@@ -362,8 +365,6 @@ int launch_hash_top1(lffn_ctx* c, const float* d_x, int64_t n, uint32_t* codes, 
     // tcgen05 3xTF32 GEMM fused with codes / coefficients (dense_tcgen05.cuh)
     DenseParams d{};
     d.x = d_x;
-    d.wt_hi = c->d_wt_hi;
-    d.wt_lo = c->d_wt_lo;
     d.wt64 = c->d_wt64;
     d.n = n;
     d.d_in = int(c->cfg.d_in);
@@ -384,10 +385,16 @@ int launch_hash_top1(lffn_ctx* c, const float* d_x, int64_t n, uint32_t* codes, 
     d.fix_cap = c->fix_cap;
     // split x into tf32 hi / lo (ctx scratch; the TMA maps are built once)
     const int64_t cnt = n * c->cfg.d_in;
-    dense_split_x_kernel<<<unsigned(std::min<int64_t>(int64_t(c->num_sms) * 8, (cnt / 4 + 255) / 256 + 1)),
-                           256, 0, st>>>(d_x, cnt, c->d_xhi, c->d_xlo, c->d_flag, c->d_fix_count);
+    const unsigned gs = unsigned(std::min<int64_t>(int64_t(c->num_sms) * 8, (cnt / 4 + 255) / 256 + 1));
+    if (c->dense_split != kSplitTf32)
+      dense_split_x_bf16x3_kernel<<<gs, 256, 0, st>>>(
+          d_x, cnt, static_cast<__nv_bfloat16*>(c->d_xp[0]), static_cast<__nv_bfloat16*>(c->d_xp[1]),
+          static_cast<__nv_bfloat16*>(c->d_xp[2]), c->d_flag, c->d_fix_count);
+    else
+      dense_split_x_kernel<<<gs, 256, 0, st>>>(d_x, cnt, static_cast<float*>(c->d_xp[0]),
+                                               static_cast<float*>(c->d_xp[1]), c->d_flag, c->d_fix_count);
     ++c->launches;
-    const size_t smem = dense_smem_bytes(d.ntile);
+    const size_t smem = dense_smem_bytes(d.ntile, c->dense_split);
 
     dim3 grid((unsigned)((d.ncols + d.ntile - 1) / d.ntile), (unsigned)((n + umma::BM - 1) / umma::BM));
     if (getenv("LFFN_DENSE_PROF")) {
@@ -399,8 +406,8 @@ int launch_hash_top1(lffn_ctx* c, const float* d_x, int64_t n, uint32_t* codes, 
       }
       d.prof = c->d_dense_prof;
     }
-    const int rc = launch_dense_tcgen05(int(c->cfg.code_bits), grid, smem, st, c->map_xhi, c->map_xlo,
-                                        c->map_whi, c->map_wlo, d);
+    const int rc = launch_dense_tcgen05(int(c->cfg.code_bits), c->dense_split, grid, smem, st,
+                                        c->dense_maps, d);
     if (rc != LFFN_OK) return rc;
     ++c->launches;
     // exact fixups: d_in <= 6144 keeps the per-warp product rows in 192 KB
@@ -831,24 +838,37 @@ int lffn_ctx_create_shard(lffn_ctx** out, int device, int64_t max_tokens, const 
     if (l <= 128 && ncols > 0 && proj->d_in % 4 == 0 && proj->d_in <= 6144) {
       // N <= 128 so the kSegs K-segment accumulators fit kTmemCols (two CTAs per SM)
       c->dense_ntile = int((128 / l) * l);
+      // operand split: bf16 x3 when the bf16 TMA rows allow it (d_in % 8 == 0;
+      // 25% fewer operand bytes, c2 dense hash 0.312 vs 0.336 ms), else tf32
+      // hi / lo (LFFN_DENSE_SPLIT=tf32 forces it)
+      c->dense_split = proj->d_in % 8 == 0 ? kSplitBf16x3 : kSplitTf32;
+      if (const char* e = getenv("LFFN_DENSE_SPLIT"))
+        if (std::string(e) == "tf32") c->dense_split = kSplitTf32;
+      const bool bf = c->dense_split != kSplitTf32;
+      const int P = bf ? 3 : 2;
+      const size_t eb = bf ? 2 : 4;
+      const uint32_t box = uint32_t(64 / eb);
       const size_t nw = size_t(ncols) * size_t(proj->d_in);
-      CK(cudaMalloc(&c->d_wt_hi, nw * sizeof(float)));
-      CK(cudaMalloc(&c->d_wt_lo, nw * sizeof(float)));
+      for (int q = 0; q < P; ++q) CK(cudaMalloc(&c->d_wp[q], nw * eb));
       CK(cudaMalloc(&c->d_wt64, nw * sizeof(double)));
-      dense_split_weights_kernel<<<unsigned((nw + 255) / 256), 256>>>(
-          c->d_W, int(proj->d_in), int(c->code_width), int(c->kb * cfg->code_bits), int(ncols),
-          c->d_wt_hi, c->d_wt_lo, c->d_wt64);
+      if (bf)
+        dense_split_weights_bf16x3_kernel<<<unsigned((nw + 255) / 256), 256>>>(
+            c->d_W, int(proj->d_in), int(c->code_width), int(c->kb * cfg->code_bits), int(ncols),
+            static_cast<__nv_bfloat16*>(c->d_wp[0]), static_cast<__nv_bfloat16*>(c->d_wp[1]),
+            static_cast<__nv_bfloat16*>(c->d_wp[2]), c->d_wt64);
+      else
+        dense_split_weights_kernel<<<unsigned((nw + 255) / 256), 256>>>(
+            c->d_W, int(proj->d_in), int(c->code_width), int(c->kb * cfg->code_bits), int(ncols),
+            static_cast<float*>(c->d_wp[0]), static_cast<float*>(c->d_wp[1]), c->d_wt64);
       CK(cudaGetLastError());
       CK(cudaDeviceSynchronize());
-      if (make_tma_map(&c->map_whi, c->d_wt_hi, uint64_t(proj->d_in), uint64_t(ncols), umma::BK,
-                       uint32_t(c->dense_ntile)) ||
-          make_tma_map(&c->map_wlo, c->d_wt_lo, uint64_t(proj->d_in), uint64_t(ncols), umma::BK,
-                       uint32_t(c->dense_ntile)))
-        c->dense_ntile = 0;  // no TMA encoder: exact float64 path
+      for (int q = 0; q < P && c->dense_ntile > 0; ++q)
+        if (make_tma_map(&c->dense_maps.w[q], c->d_wp[q], uint64_t(proj->d_in), uint64_t(ncols), box,
+                         uint32_t(c->dense_ntile), bf))
+          c->dense_ntile = 0;  // no TMA encoder: exact float64 path
       if (c->dense_ntile > 0) {
         const size_t nx = size_t(std::max<int64_t>(max_tokens, 1)) * size_t(proj->d_in);
-        CK(cudaMalloc(&c->d_xhi, nx * sizeof(float)));
-        CK(cudaMalloc(&c->d_xlo, nx * sizeof(float)));
+        for (int q = 0; q < P; ++q) CK(cudaMalloc(&c->d_xp[q], nx * eb));
         // |z| < 1e-4 is ~1e-4 of the z for Gaussian-like projections; 1M
         // entries (8 MB) covers 4096 x 2048 all-candidate tiles before the
         // kernel falls back to inline recomputation
@@ -856,11 +876,10 @@ int lffn_ctx_create_shard(lffn_ctx** out, int device, int64_t max_tokens, const 
         CK(cudaMalloc(&c->d_fix_list, size_t(c->fix_cap) * sizeof(uint2)));
         CK(cudaMalloc(&c->d_fix_count, sizeof(int)));
         CK(cudaMemset(c->d_fix_count, 0, sizeof(int)));
-        if (make_tma_map(&c->map_xhi, c->d_xhi, uint64_t(proj->d_in), uint64_t(std::max<int64_t>(max_tokens, 1)),
-                         umma::BK, umma::BM) ||
-            make_tma_map(&c->map_xlo, c->d_xlo, uint64_t(proj->d_in), uint64_t(std::max<int64_t>(max_tokens, 1)),
-                         umma::BK, umma::BM))
-          c->dense_ntile = 0;
+        for (int q = 0; q < P && c->dense_ntile > 0; ++q)
+          if (make_tma_map(&c->dense_maps.x[q], c->d_xp[q], uint64_t(proj->d_in),
+                           uint64_t(std::max<int64_t>(max_tokens, 1)), box, umma::BM, bf))
+            c->dense_ntile = 0;
       }
     }
     if (const char* e = getenv("LFFN_DENSE_EXACT")) c->dense_exact = atoi(e);
