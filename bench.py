@@ -373,6 +373,8 @@ def run_ours(args):
         g = C.c_double()
         _capi.check(_capi.lib().lffn_probe_bandwidth(local, 0, 5, C.byref(g)))
         l2 = g.value
+        _capi.check(_capi.lib().lffn_probe_bandwidth(local, 2, 5, C.byref(g)))
+        l2_rand = g.value
         gather_avg = float(np.mean(gather_ms))
         hash_avg = float(np.mean(hash_ms))
         t_roof_ms = (U / (hbm * 1e9) + G / (l2 * 1e9)) * 1e3
@@ -435,6 +437,11 @@ def run_ours(args):
                 "bw_l2_gbs": round(l2, 1),
                 "bw_l2_source": "measured live (lffn_probe_bandwidth, 32 MiB re-read)",
                 "t_roof_ms": round(t_roof_ms, 5),
+                # context, not the denominator: the same probe with the
+                # gather's access pattern (random 512-byte segments)
+                "bw_l2_random_512B_gbs": round(l2_rand, 1),
+                "frac_vs_random_segment_l2": round(
+                    (U / (hbm * 1e9) + G / (l2_rand * 1e9)) * 1e3 / gather_avg, 4),
                 "hbm_frac_unique": round((U + x.nbytes + n * cfg.d_out * 4) /
                                          (gather_avg * 1e-3 + hash_avg * 1e-3) / 1e9 / hbm, 4),
             },

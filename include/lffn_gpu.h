@@ -216,9 +216,19 @@ int lffn_sync(lffn_ctx* ctx, void* stream);
  *                              exact float64 recomputation of |z| < 1e-4, so
  *                              codes stay bit-exact
  *   LFFN_OPT_TABLE_GROUP_BYTES walk the tables in L2-sized groups of this many
- *                              bytes (0 = one pass, the default) */
+ *                              bytes (0 = one pass, the default)
+ *   LFFN_OPT_GATHER_VARIANT    gather kernel: 0 = default (batches smaller
+ *                              than the resident warp slots split each
+ *                              token's table walk over 2-8 warps), -1 = one
+ *                              warp per token (part) always
+ *   LFFN_OPT_FUSED             0 (default) = hash kernel, then gather kernel;
+ *                              1 = both in one warp-specialised persistent
+ *                              kernel where the shape allows (signflip,
+ *                              D = 2048; measured slower, for A/B) */
 #define LFFN_OPT_DENSE_EXACT 1
 #define LFFN_OPT_TABLE_GROUP_BYTES 2
+#define LFFN_OPT_GATHER_VARIANT 3
+#define LFFN_OPT_FUSED 4
 int lffn_ctx_set_option(lffn_ctx* ctx, int option, int64_t value);
 
 /* Number of kernels launched through this context since creation. */
@@ -232,7 +242,8 @@ int lffn_ctx_stage_ms(lffn_ctx* ctx, float* hash_ms, float* gather_ms);
 
 /* Bandwidth probe for the roofline denominators (no reference counterpart):
  * which = 0 L2 read GB/s (32 MiB re-read from every SM), 1 HBM read GB/s
- * (4 GiB stream); best of reps CUDA-event-timed launches. */
+ * (4 GiB stream), 2 L2 read GB/s of random 512-byte segments of a 32 MiB
+ * buffer (the gather's pattern); best of reps CUDA-event-timed launches. */
 int lffn_probe_bandwidth(int device, int which, int reps, double* gbs);
 
 /* Thread-local message for the last non-zero status. */

@@ -404,3 +404,115 @@ __global__ void __launch_bounds__(256, MINB) gather_row_persistent_kernel(Gather
 }
 
 }  // namespace lffn_gpu
+
+namespace lffn_gpu {
+
+// Split-table gather for batches smaller than the resident warp slots (small
+// serving batches, the host path's pipeline chunks): S warps of a CTA share
+// one (token, column part) and each walks a contiguous 1/S of the tables
+// (ascending, TIF tables' 128-bit row segments in flight per lane), so the
+// per-token chain of dependent table rounds is S times shorter.  The S fp32
+// partials meet in shared memory and are summed in split order (tables
+// ascending within each split) -- deterministic, no atomics.  A CTA of 256
+// threads holds 8 / S items.  Requires the 4-record layout with
+// (nk / S) % 4 == 0 and 16-byte aligned rows.
+template <typename TT, int MAXC, int TIF, int S>
+__global__ void __launch_bounds__(256, 2) gather_split_kernel(GatherParams p, int parts) {
+  constexpr int VEC = Raw<TT>::VEC;
+  constexpr int CHUNK = 32 * VEC;
+  constexpr int IPC = 8 / S;  // items per CTA
+  __shared__ float4 part_sm[8][MAXC][VEC / 4][32];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int split = wib % S;
+  const int64_t item = (int64_t)blockIdx.x * IPC + wib / S;
+  const int nchunks = (p.d_out + CHUNK - 1) / CHUNK;
+  const bool live = item < p.n * parts;
+  const int64_t token = live ? item / parts : 0;
+  const int part = live ? (int)(item - token * parts) : 0;
+  const int c0 = part * MAXC;
+  const int colbase = c0 * CHUNK + lane * VEC;
+  bool ok[MAXC];
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c) ok[c] = live && (c0 + c < nchunks) && (colbase + c * CHUNK < p.d_out);
+  const TT* T = reinterpret_cast<const TT*>(p.T);
+  const int64_t tstride = (int64_t)p.rows * p.d_out;
+  const int per = p.nk / S;
+  const int kb = split * per;
+  const uint32_t* cr = p.codes + token * p.ld + kb;
+  const float* wr = p.coeff + token * p.ld + kb;
+  float acc[MAXC][VEC];
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c)
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) acc[c][v] = 0.f;
+  if (live) {
+    uint4 cc = __ldg(reinterpret_cast<const uint4*>(cr));
+    float4 ww = __ldg(reinterpret_cast<const float4*>(wr));
+    for (int it = 0; it < per; it += 4) {
+      uint4 cn = cc;
+      float4 wn = ww;
+      if (it + 4 < per) {
+        cn = __ldg(reinterpret_cast<const uint4*>(cr + it + 4));
+        wn = __ldg(reinterpret_cast<const float4*>(wr + it + 4));
+      }
+      const uint32_t code4[4] = {cc.x, cc.y, cc.z, cc.w};
+      const float w4[4] = {ww.x, ww.y, ww.z, ww.w};
+#pragma unroll
+      for (int q0 = 0; q0 < 4; q0 += TIF) {
+        uint4 raw[TIF][MAXC];
+#pragma unroll
+        for (int q = 0; q < TIF; ++q) {
+          const TT* rp = T + (int64_t)(kb + it + q0 + q) * tstride + (int64_t)code4[q0 + q] * p.d_out + colbase;
+#pragma unroll
+          for (int c = 0; c < MAXC; ++c)
+            raw[q][c] = ok[c] ? Raw<TT>::load(rp + c * CHUNK) : make_uint4(0u, 0u, 0u, 0u);
+        }
+#pragma unroll
+        for (int q = 0; q < TIF; ++q)
+#pragma unroll
+          for (int c = 0; c < MAXC; ++c) Raw<TT>::fma(acc[c], w4[q0 + q], raw[q][c]);
+      }
+      cc = cn;
+      ww = wn;
+    }
+  }
+  if (split != 0) {
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c)
+#pragma unroll
+      for (int v = 0; v < VEC; v += 4)
+        part_sm[wib][c][v / 4][lane] = make_float4(acc[c][v], acc[c][v + 1], acc[c][v + 2], acc[c][v + 3]);
+  }
+  __syncthreads();
+  if (split != 0 || !live) return;
+#pragma unroll
+  for (int s = 1; s < S; ++s)
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c)
+#pragma unroll
+      for (int v = 0; v < VEC; v += 4) {
+        const float4 q = part_sm[wib + s][c][v / 4][lane];
+        acc[c][v] += q.x; acc[c][v + 1] += q.y; acc[c][v + 2] += q.z; acc[c][v + 3] += q.w;
+      }
+  int bad = 0;
+  float* yr = p.y + token * p.d_out;
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c) {
+    if (!ok[c]) continue;
+    const int col = colbase + c * CHUNK;
+#pragma unroll
+    for (int v = 0; v < VEC; v += 4) {
+      float4 o = make_float4(acc[c][v], acc[c][v + 1], acc[c][v + 2], acc[c][v + 3]);
+      if (p.accumulate) {
+        const float4 a = *reinterpret_cast<const float4*>(yr + col + v);
+        o.x += a.x; o.y += a.y; o.z += a.z; o.w += a.w;
+      }
+      if (!isfinite(o.x) || !isfinite(o.y) || !isfinite(o.z) || !isfinite(o.w)) bad = 4;
+      *reinterpret_cast<float4*>(yr + col + v) = o;
+    }
+  }
+  if (bad) atomicOr(p.flag, bad);
+}
+
+}  // namespace lffn_gpu

@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "gather_kernels.cuh"
+#include "fused_kernels.cuh"
 #include "hash_kernels.cuh"
 #include "dense_tcgen05.cuh"
 #include "hash_bh_kernel.cuh"
@@ -104,6 +105,8 @@ struct lffn_ctx {
   int64_t launches = 0;
   int num_sms = 148;
   size_t table_group_bytes = 0;  // >0: walk tables in groups of this many bytes (measured slower on c2)
+  int64_t gather_variant = 0;    // LFFN_OPT_GATHER_VARIANT (0 = default choice)
+  int fused = 0;                 // LFFN_OPT_FUSED: 1 = one-kernel hash + gather (opt-in)
 };
 
 namespace {
@@ -115,6 +118,7 @@ int flag_message(int flag) {
   if (flag & kFlagBwdInput) return fail(LFFN_ERR_NUMERIC, "non-finite values in lookup backward input");
   if (flag & kFlagBwdOutput) return fail(LFFN_ERR_NUMERIC, "non-finite values in projection backward output");
   if (flag & kFlagBwdTables) return fail(LFFN_ERR_NUMERIC, "non-finite values in lookup backward tables");
+  if (flag & kFlagStream) return fail(LFFN_ERR_RUNTIME, "host pipeline: device wait for an input copy timed out");
   return LFFN_OK;
 }
 
@@ -303,6 +307,23 @@ int launch_hash(lffn_ctx* c, const float* d_x, int64_t n, uint32_t* codes, float
   ++c->launches;
   LFFN_CUDA(cudaGetLastError());
   return LFFN_OK;
+}
+
+void fill_hash_params(const lffn_ctx* c, HashParams& p, const float* d_x, int64_t n) {
+  p.x = d_x;
+  p.n = n;
+  p.d_in = int(c->cfg.d_in);
+  p.D = int(c->D);
+  p.logD = int(c->logD);
+  p.code_width = int(c->code_width);
+  p.tau = int(c->cfg.code_bits);
+  p.kb = int(c->kb);
+  p.ke = int(c->ke);
+  p.scaled = (c->cfg.variant == LFFN_SCALED || c->cfg.variant == LFFN_GELU_TAU1) ? 1 : 0;
+  p.n_transforms = c->n_transforms;
+  p.signmask = c->d_signmask;
+  p.diag = c->d_diag;
+  p.flag = c->d_flag;
 }
 
 int launch_hash_top1(lffn_ctx* c, const float* d_x, int64_t n, uint32_t* codes, float* coeff,
@@ -556,6 +577,33 @@ int launch_gather_group(lffn_ctx* c, const uint32_t* codes, const float* coeff, 
       const int64_t pwarps = n * pwpt;
       const unsigned pgrid = (unsigned)std::min<int64_t>(int64_t(c->num_sms) * 2, (pwarps * 32 + 255) / 256);
       (void)pg;
+      // fewer (token, part) items than resident warp slots: split the table
+      // walk over S warps per item (gather_split_kernel), S the largest of
+      // 8/4/2 that keeps n*parts*S within the slots
+      const int64_t slots = int64_t(c->num_sms) * 16;
+      int S = 1;
+      if (c->gather_variant == 0) {
+        for (int s : {8, 4, 2})
+          if (pwarps * s <= slots && p.nk % (4 * s) == 0) { S = s; break; }
+      }
+      if (S > 1) {
+        const unsigned sgrid = (unsigned)((pwarps * S + 7) / 8);
+#define LFFN_SPLIT(TT, M)                                                                   \
+  if (S == 8) gather_split_kernel<TT, M, 4, 8><<<sgrid, 256, 0, st>>>(p, pwpt);             \
+  else if (S == 4) gather_split_kernel<TT, M, 4, 4><<<sgrid, 256, 0, st>>>(p, pwpt);        \
+  else gather_split_kernel<TT, M, 4, 2><<<sgrid, 256, 0, st>>>(p, pwpt);
+        if (f32) {
+          if (pmaxc == 2) { LFFN_SPLIT(float, 2) } else if (pmaxc == 4) { LFFN_SPLIT(float, 4) }
+          else { LFFN_SPLIT(float, 6) }
+        } else {
+          if (pmaxc == 2) { LFFN_SPLIT(__nv_bfloat16, 2) } else if (pmaxc == 3) { LFFN_SPLIT(__nv_bfloat16, 3) }
+          else { LFFN_SPLIT(__nv_bfloat16, 4) }
+        }
+#undef LFFN_SPLIT
+        ++c->launches;
+        LFFN_CUDA(cudaGetLastError());
+        return LFFN_OK;
+      }
       // (measured at c2 fp32: one warp per token with 6 chunks and 2 CTAs/SM
       // beats 2-3 warps per token at 3-4 CTAs/SM, 0.641 vs 0.698-0.942 ms;
       // L2 evict_last/evict_first splits of the table stack: 0.68-0.81 ms)
@@ -637,9 +685,105 @@ int launch_gather(lffn_ctx* c, const uint32_t* codes, const float* coeff, int64_
   return LFFN_OK;
 }
 
+// K13: hash + gather in one persistent kernel (fused_kernels.cuh) for the
+// signflip projection at D = 2048 with tau 8 / 10 (BASELINE c2, c3, c5).
+// Returns 1 (nothing launched) when the shape is not covered.
+using FusedFn = void (*)(FusedParams);
+struct FusedChoice {
+  FusedFn fn = nullptr;
+  int maxc = 0, block = 128;
+  int hp = 0, ring = 0;  // warp-specialised kernel: hash pairs, ring slots (0 = same-warp kernel)
+};
+
+// LFFN_OPT_FUSED 1: warp-specialised fused_ws_kernel (opt-in: measured
+// slower than the two kernels, fused_kernels.cuh)
+FusedChoice fused_choice(const lffn_ctx* c) {
+  FusedChoice f;
+  if (!c->fused || c->nc != 1 || c->proj.kind != LFFN_PROJ_SIGNFLIP || c->n_transforms != 3 ||
+      c->logD != 11 || c->h_loc == 0 || c->h_loc % 4 != 0)
+    return f;
+  const int tau = int(c->cfg.code_bits);
+  const int64_t d_out = c->cfg.d_out;
+  const bool f32 = c->t_dtype == LFFN_F32;
+  if (d_out % (f32 ? 4 : 8) != 0) return f;
+  const int64_t nchunks = (d_out + (f32 ? 128 : 256) - 1) / (f32 ? 128 : 256);
+  static const int hp = getenv("LFFN_FUSED_HP") ? atoi(getenv("LFFN_FUSED_HP")) : 2;
+  constexpr int R = 32;
+#define LFFN_WS(TT, TAU, M)                                                          \
+  (hp == 3 ? FusedChoice{&fused_ws_kernel<TT, TAU, M, 3, R>, M, 512, 3, R}           \
+             : FusedChoice{&fused_ws_kernel<TT, TAU, M, 2, R>, M, 512, 2, R})
+  if (f32 && tau == 8 && nchunks == 6) f = LFFN_WS(float, 8, 6);
+  else if (!f32 && tau == 8 && nchunks == 3) f = LFFN_WS(__nv_bfloat16, 8, 3);
+  else if (!f32 && tau == 10 && nchunks == 4) f = LFFN_WS(__nv_bfloat16, 10, 4);
+#undef LFFN_WS
+  if (int64_t(c->h_loc) * 8 * f.ring > 160 * 1024) f = FusedChoice{};  // ring must fit
+  return f;
+}
+
+// fills the hash / gather halves of FusedParams as the two-kernel path would
+void fill_hash_params(const lffn_ctx* c, HashParams& p, const float* d_x, int64_t n);
+
+int launch_fused(lffn_ctx* c, const FusedChoice& f, const float* d_x, int64_t n, float* d_y,
+                 const int* ready, int* done, int64_t chunk_tokens, cudaStream_t st) {
+  FusedParams fp{};
+  fill_hash_params(c, fp.h, d_x, n);
+  GatherParams& g = fp.g;
+  g.T = c->d_T;
+  g.y = d_y;
+  g.n = n;
+  g.ld = int(c->h_loc);
+  g.nk = int(c->h_loc);
+  g.nc = 1;
+  g.rows = int(c->rows);
+  g.d_out = int(c->cfg.d_out);
+  g.flag = c->d_flag;
+  const int chunk = c->t_dtype == LFFN_F32 ? 128 : 256;
+  const int nchunks = int((c->cfg.d_out + chunk - 1) / chunk);
+  fp.parts = (nchunks + f.maxc - 1) / f.maxc;
+  fp.ready = ready;
+  fp.done = done;
+  fp.chunk_tokens = chunk_tokens > 0 ? chunk_tokens : n;
+  fp.spin_limit = int64_t(1) << 24;  // ~4 s of 256 ns sleeps
+  static const int dbg = getenv("LFFN_FUSED_DEBUG") ? atoi(getenv("LFFN_FUSED_DEBUG")) : 0;
+  fp.debug_mode = dbg;
+  size_t smem;
+  unsigned grid;
+  if (f.hp > 0) {
+    // one 16-warp CTA per SM, each owning a contiguous token range
+    const size_t slot = size_t((c->h_loc * 8 + 15) / 16 * 16);
+    smem = size_t(16) * f.ring + size_t(f.hp) * size_t(padded_len(int(c->D))) * sizeof(double) +
+           size_t(f.ring) * slot;
+    grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(int64_t(c->num_sms), (n + 15) / 16)));
+  } else {
+    return fail(LFFN_ERR_USAGE, "fused forward: no kernel for this shape");
+  }
+  LFFN_CUDA(cudaFuncSetAttribute(f.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  f.fn<<<grid, f.block, smem, st>>>(fp);
+  ++c->launches;
+  LFFN_CUDA(cudaGetLastError());
+  return LFFN_OK;
+}
+
+// the fused kernel runs one warp per token: below ~2 rounds of resident
+// warps the split gather (several warps per token) finishes first
+bool use_fused(const lffn_ctx* c, int64_t n) {
+  static const int64_t min_n = getenv("LFFN_FUSED_MIN_TOKENS") ? atol(getenv("LFFN_FUSED_MIN_TOKENS")) : 4096;
+  return n >= min_n && fused_choice(c).fn != nullptr && c->d_T != nullptr;
+}
+
 int forward_impl(lffn_ctx* c, const float* d_x, int64_t n, float* d_y, cudaStream_t st) {
   const bool tm = c->timing;
   if (tm) LFFN_CUDA(cudaEventRecord(c->ev_t0, st));
+  if (use_fused(c, n)) {
+    // one kernel: the whole forward is reported as the gather stage
+    if (tm) LFFN_CUDA(cudaEventRecord(c->ev_t1, st));
+    if (int rc = launch_fused(c, fused_choice(c), d_x, n, d_y, nullptr, nullptr, 0, st)) return rc;
+    if (tm) {
+      LFFN_CUDA(cudaEventRecord(c->ev_t2, st));
+      c->timed = true;
+    }
+    return LFFN_OK;
+  }
   if (int rc = launch_hash(c, d_x, n, c->d_codes, c->d_coeff, nullptr, st)) return rc;
   if (tm) LFFN_CUDA(cudaEventRecord(c->ev_t1, st));
   if (int rc = launch_gather(c, c->d_codes, c->d_coeff, n, d_y, 0, st)) return rc;
@@ -1351,6 +1495,15 @@ int lffn_ctx_set_option(lffn_ctx* c, int option, int64_t value) {
   switch (option) {
     case LFFN_OPT_DENSE_EXACT:
       c->dense_exact = value != 0;
+      return LFFN_OK;
+    case LFFN_OPT_GATHER_VARIANT:
+      if (value != 0 && value != -1)
+        return fail(LFFN_ERR_USAGE, "option: no such gather variant " + std::to_string(value));
+      c->gather_variant = value;
+      return LFFN_OK;
+    case LFFN_OPT_FUSED:
+      if (value < 0 || value > 1) return fail(LFFN_ERR_USAGE, "option: fused must be 0 or 1");
+      c->fused = int(value);
       return LFFN_OK;
     case LFFN_OPT_TABLE_GROUP_BYTES:
       if (value < 0) return fail(LFFN_ERR_USAGE, "option: negative table group size");

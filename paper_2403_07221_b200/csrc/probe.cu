@@ -46,12 +46,35 @@ __global__ void hbm_read_kernel(const float4* __restrict__ p, size_t n4, float* 
   if (acc == 1234.5f) *out = acc;
 }
 
+// Random 512-byte segments (one per warp load, 32 x 16 B) of an L2-resident
+// buffer: the gather's access granularity without its arithmetic.  Every
+// lane keeps 8 independent segments in flight.
+__global__ void l2_random_kernel(const float4* __restrict__ p, uint32_t nseg_mask, int iters,
+                                 float* out) {
+  const int lane = threadIdx.x & 31;
+  uint32_t h = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  h = h * 2654435761u + 12345u;
+  float acc = 0.f;
+  for (int it = 0; it < iters; ++it) {
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      h ^= h << 13; h ^= h >> 17; h ^= h << 5;  // xorshift, warp-uniform
+      v[u] = __ldg(p + (size_t)(h & nseg_mask) * 32 + lane);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += v[u].x + v[u].y + v[u].z + v[u].w;
+  }
+  if (acc == 1234.5f) *out = acc;
+}
+
 }  // namespace
 
 extern "C" {
 
-// which = 0: L2 read bandwidth (32 MiB working set), 1: HBM read bandwidth
-// (4 GiB stream).  Best of `reps` timed launches, GB/s of bytes loaded.
+// which = 0: L2 read bandwidth (32 MiB working set, sequential 128-bit
+// re-reads), 1: HBM read bandwidth (4 GiB stream), 2: L2 read bandwidth
+// for random 512-byte segments of a 32 MiB buffer (the gather's pattern).  Best of `reps` timed launches, GB/s of bytes loaded.
 int lffn_probe_bandwidth(int device, int which, int reps, double* gbs) {
   using lffn_gpu::fail;
   if (!gbs) return fail(LFFN_ERR_USAGE, "probe: null output");
@@ -62,7 +85,7 @@ int lffn_probe_bandwidth(int device, int which, int reps, double* gbs) {
   if (cudaGetDeviceProperties(&prop, device) != cudaSuccess)
     return fail(LFFN_ERR_RUNTIME, "probe: no device");
   const int sms = prop.multiProcessorCount;
-  const size_t bytes = which == 0 ? (size_t(32) << 20) : (size_t(4) << 30);
+  const size_t bytes = which == 1 ? (size_t(4) << 30) : (size_t(32) << 20);
   void* buf = nullptr;
   float* out = nullptr;
   cudaEvent_t a, b;
@@ -75,7 +98,11 @@ int lffn_probe_bandwidth(int device, int which, int reps, double* gbs) {
   const int passes = 16;
   for (int r = 0; r < reps + 1; ++r) {
     cudaEventRecord(a);
-    if (which == 0)
+    const int rit = 64;
+    if (which == 2)
+      l2_random_kernel<<<sms * 2, 1024>>>(static_cast<const float4*>(buf), uint32_t(bytes / 512 - 1),
+                                          rit, out);
+    else if (which == 0)
       l2_read_kernel<<<sms * 2, 1024>>>(static_cast<const float4*>(buf), bytes / 16 - 1, passes,
                                         out);
     else
@@ -84,7 +111,9 @@ int lffn_probe_bandwidth(int device, int which, int reps, double* gbs) {
     cudaEventSynchronize(b);
     float ms = 0.f;
     cudaEventElapsedTime(&ms, a, b);
-    const double moved = which == 0 ? double(bytes) * passes * sms * 2 : double(bytes);
+    const double moved = which == 0 ? double(bytes) * passes * sms * 2
+                         : which == 2 ? double(sms) * 2 * 32 * rit * 8 * 512.0
+                                      : double(bytes);
     if (r > 0 && ms > 0.f) best = std::max(best, moved / (ms * 1e6));
   }
   const cudaError_t e = cudaGetLastError();

@@ -444,9 +444,13 @@ class LookupFFN:
 
     def set_option(self, name: str, value: int) -> None:
         """'dense_exact' (exact float64 dense projection instead of the
-        tcgen05 3xTF32 GEMM) or 'table_group_bytes'."""
+        tcgen05 split-precision GEMM), 'table_group_bytes', 'gather_variant'
+        (0 default, -1 one warp per token always) or 'fused' (1 = the opt-in
+        one-kernel hash + gather)."""
         opt = {"dense_exact": _capi.LFFN_OPT_DENSE_EXACT,
-               "table_group_bytes": _capi.LFFN_OPT_TABLE_GROUP_BYTES}[name]
+               "table_group_bytes": _capi.LFFN_OPT_TABLE_GROUP_BYTES,
+               "gather_variant": _capi.LFFN_OPT_GATHER_VARIANT,
+               "fused": _capi.LFFN_OPT_FUSED}[name]
         check(_capi.lib().lffn_ctx_set_option(self._ctx, opt, int(value)))
 
     def launch_count(self) -> int:
