@@ -224,11 +224,17 @@ int lffn_sync(lffn_ctx* ctx, void* stream);
  *   LFFN_OPT_FUSED             0 (default) = hash kernel, then gather kernel;
  *                              1 = both in one warp-specialised persistent
  *                              kernel where the shape allows (signflip,
- *                              D = 2048; measured slower, for A/B) */
+ *                              D = 2048; measured slower, for A/B)
+ *   LFFN_OPT_BF16_COEFF_FMA    1 (default) = bf16 tables: groups of tables
+ *                              whose coefficients are bf16 values (e.g. the
+ *                              top-1 weight 1.0) accumulate with the exact
+ *                              mixed-precision FMA on the packed halves (bit-
+ *                              identical to the fp32 FMA); 0 = always unpack */
 #define LFFN_OPT_DENSE_EXACT 1
 #define LFFN_OPT_TABLE_GROUP_BYTES 2
 #define LFFN_OPT_GATHER_VARIANT 3
 #define LFFN_OPT_FUSED 4
+#define LFFN_OPT_BF16_COEFF_FMA 5
 int lffn_ctx_set_option(lffn_ctx* ctx, int option, int64_t value);
 
 /* Number of kernels launched through this context since creation. */

@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(HERE, "csrc", "liblffn_gpu.so")
 LFFN_OK, LFFN_ERR_USAGE, LFFN_ERR_NUMERIC, LFFN_ERR_RUNTIME = 0, 1, 2, 3
 LFFN_F32, LFFN_BF16, LFFN_F64 = 0, 1, 2
 LFFN_OPT_DENSE_EXACT, LFFN_OPT_TABLE_GROUP_BYTES, LFFN_OPT_GATHER_VARIANT, LFFN_OPT_FUSED = 1, 2, 3, 4
+LFFN_OPT_BF16_COEFF_FMA = 5
 
 
 class lffn_cfg(C.Structure):

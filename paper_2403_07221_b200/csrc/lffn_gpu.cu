@@ -107,6 +107,7 @@ struct lffn_ctx {
   size_t table_group_bytes = 0;  // >0: walk tables in groups of this many bytes (measured slower on c2)
   int64_t gather_variant = 0;    // LFFN_OPT_GATHER_VARIANT (0 = default choice)
   int fused = 0;                 // LFFN_OPT_FUSED: 1 = one-kernel hash + gather (opt-in)
+  int bf16w = 1;                 // LFFN_OPT_BF16_COEFF_FMA: exact FHFMA path for bf16 tables
 };
 
 namespace {
@@ -548,9 +549,12 @@ int launch_gather_group(lffn_ctx* c, const uint32_t* codes, const float* coeff, 
   p.d_out = int(c->cfg.d_out);
   p.accumulate = accumulate;
   p.flag = c->d_flag;
+  p.bf16w = c->bf16w;
   // odd rounds of resident tokens walk the tables backwards (the tables the
-  // previous round finished with are still in L2): measured +2.5% (c2 bf16),
-  // +6% (c3), +1.5% (c4) for bf16 tables, -2% for c2 fp32
+  // previous round finished with are still in L2): with the exact bf16-
+  // coefficient FMA, measured +4% (c2 bf16) and +4% (c3) for bf16 tables
+  // walked one warp per token, -6% for c4 (four warps per token,
+  // part-major) and -2% for c2 fp32; set per launch below
   static const int rev = getenv("LFFN_GATHER_REVERSE") ? atoi(getenv("LFFN_GATHER_REVERSE")) : -1;
   p.reverse_odd_rounds = rev >= 0 ? rev : (c->t_dtype == LFFN_BF16 ? 1 : 0);
   const bool f32 = c->t_dtype == LFFN_F32;
@@ -572,9 +576,18 @@ int launch_gather_group(lffn_ctx* c, const uint32_t* codes, const float* coeff, 
       const unsigned pg = (unsigned)std::min<int64_t>(int64_t(c->num_sms) * 2, (warps * 32 + 255) / 256);
       // (MAXC 2 for bf16 -- 2x the column parts, half the bytes in flight per
       // warp -- measured slower: c3 1.39 vs 1.22 ms, c4 2.47 vs 2.07 ms)
-      const int pmaxc = f32 ? maxc : (nchunks <= 2 ? 2 : nchunks <= 3 ? 3 : 4);
+      int pmaxc = f32 ? maxc : (nchunks <= 2 ? 2 : nchunks <= 3 ? 3 : 4);
+      int ptif = 4;
+      static const char* bcfg = getenv("LFFN_GATHER_BF16_CFG");  // tuning: "MAXC,TIF"
+      if (!f32 && bcfg) {
+        int m = 0, t = 0;
+        if (sscanf(bcfg, "%d,%d", &m, &t) == 2 && ((m == 2 && t == 8) || (m == 1 && t == 8) ||
+                                                   (m == 4 && t == 2) || (m == 2 && t == 4)))
+          pmaxc = m, ptif = t;
+      }
       const int pwpt = (nchunks + pmaxc - 1) / pmaxc;
       const int64_t pwarps = n * pwpt;
+      if (rev < 0 && pwpt > 1) p.reverse_odd_rounds = 0;
       const unsigned pgrid = (unsigned)std::min<int64_t>(int64_t(c->num_sms) * 2, (pwarps * 32 + 255) / 256);
       (void)pg;
       // fewer (token, part) items than resident warp slots: split the table
@@ -620,7 +633,10 @@ int launch_gather_group(lffn_ctx* c, const uint32_t* codes, const float* coeff, 
         if (pmaxc == 2) { LFFN_PROW(float, 2, 4) } else if (pmaxc == 4) { LFFN_PROW(float, 4, 4) }
         else { LFFN_PROW(float, 6, 4) }
       } else {
-        if (pmaxc == 2) { LFFN_PROW(__nv_bfloat16, 2, 4) } else if (pmaxc == 3) { LFFN_PROW(__nv_bfloat16, 3, 4) } else { LFFN_PROW(__nv_bfloat16, 4, 4) }
+        if (pmaxc == 2 && ptif == 8) { LFFN_PROW(__nv_bfloat16, 2, 8) }
+        else if (pmaxc == 1) { LFFN_PROW(__nv_bfloat16, 1, 8) }
+        else if (pmaxc == 4 && ptif == 2) { LFFN_PROW(__nv_bfloat16, 4, 2) }
+        else if (pmaxc == 2) { LFFN_PROW(__nv_bfloat16, 2, 4) } else if (pmaxc == 3) { LFFN_PROW(__nv_bfloat16, 3, 4) } else { LFFN_PROW(__nv_bfloat16, 4, 4) }
       }
 #undef LFFN_PROW
       ++c->launches;
@@ -1504,6 +1520,9 @@ int lffn_ctx_set_option(lffn_ctx* c, int option, int64_t value) {
     case LFFN_OPT_FUSED:
       if (value < 0 || value > 1) return fail(LFFN_ERR_USAGE, "option: fused must be 0 or 1");
       c->fused = int(value);
+      return LFFN_OK;
+    case LFFN_OPT_BF16_COEFF_FMA:
+      c->bf16w = value != 0;
       return LFFN_OK;
     case LFFN_OPT_TABLE_GROUP_BYTES:
       if (value < 0) return fail(LFFN_ERR_USAGE, "option: negative table group size");

@@ -445,12 +445,14 @@ class LookupFFN:
     def set_option(self, name: str, value: int) -> None:
         """'dense_exact' (exact float64 dense projection instead of the
         tcgen05 split-precision GEMM), 'table_group_bytes', 'gather_variant'
-        (0 default, -1 one warp per token always) or 'fused' (1 = the opt-in
-        one-kernel hash + gather)."""
+        (0 default, -1 one warp per token always), 'fused' (1 = the opt-in
+        one-kernel hash + gather) or 'bf16_coeff_fma' (0 = never take the
+        exact mixed-precision FMA path for bf16 tables)."""
         opt = {"dense_exact": _capi.LFFN_OPT_DENSE_EXACT,
                "table_group_bytes": _capi.LFFN_OPT_TABLE_GROUP_BYTES,
                "gather_variant": _capi.LFFN_OPT_GATHER_VARIANT,
-               "fused": _capi.LFFN_OPT_FUSED}[name]
+               "fused": _capi.LFFN_OPT_FUSED,
+               "bf16_coeff_fma": _capi.LFFN_OPT_BF16_COEFF_FMA}[name]
         check(_capi.lib().lffn_ctx_set_option(self._ctx, opt, int(value)))
 
     def launch_count(self) -> int:

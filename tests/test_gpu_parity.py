@@ -441,3 +441,37 @@ def test_fused_ws_kernel_matches_two_kernels(oracle, name, n):
     y_ref = oracle.lookup_forward(c, s, proj.blob, stored_tables(T.data, w.table_dtype),
                                   x.astype(np.float64))
     assert_close(y1, y_ref, FP32_TOL, "fused vs oracle")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,n", [("c2_bf16", 3000), ("c2_bf16", 40), ("c3", 2500)])
+def test_bf16_coeff_fma_path_bit_identical(name, n):
+    """bf16 tables: groups of four tables whose coefficients are bf16 values
+    take the mixed-precision FMA on the packed halves; the products are exact,
+    so y is bit-identical to the unpack + fp32 FMA path.  Coefficients mix
+    1.0, other bf16 values and general fp32 values so both paths and the
+    switch between them run inside one table walk (persistent and split
+    kernels)."""
+    import torch
+
+    w = WORKLOADS[name]
+    cfg, proj, T = make_params(w)
+    layer = LookupFFN(cfg, proj, T, max_tokens=n, table_dtype=w.table_dtype)
+    g = torch.Generator().manual_seed(7)
+    codes = torch.randint(0, 1 << w.tau, (n, w.h), generator=g, dtype=torch.int32)
+    coeff = torch.ones((n, w.h), dtype=torch.float32)
+    pick = torch.rand((n, w.h), generator=g)
+    gen = torch.rand((n, w.h), generator=g) * 2 - 1
+    coeff = torch.where(pick < 0.15, gen, coeff)                       # general fp32
+    coeff = torch.where(pick > 0.9, gen.to(torch.bfloat16).float(), coeff)  # bf16 values
+    codes, coeff = codes.cuda(), coeff.cuda()
+    outs = []
+    for on in (1, 0):
+        layer.set_option("bf16_coeff_fma", on)
+        for acc in (False, True):
+            y = torch.full((n, cfg.d_out), 0.5, device="cuda")
+            layer.lookup_accumulate(codes, coeff, y, accumulate=acc)
+            layer.sync()
+            outs.append(y.cpu().numpy())
+    assert np.array_equal(outs[0], outs[2])
+    assert np.array_equal(outs[1], outs[3])

@@ -34,3 +34,14 @@ echo "prof dense rc=$?"
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"gather_row" -s 1 -c 1 \
   -o $out/${tag}_prof_c4 -f python bench.py --config c4 --steps 1 --warmup 3 --no-cpu-baseline > $out/${tag}_ncu_c4.log 2>&1
 echo "prof c4 rc=$?"
+# summaries on the box (the .ncu-rep files together exceed gpurun's 64 MiB
+# copy-back limit): markdown + raw CSV pages, then keep only the c2 capture
+python tools/ncu_summary.py launches $out/${tag}_launches.csv > $out/${tag}_launches.md 2>&1
+for r in prof prof_dense prof_c4; do
+  python tools/ncu_summary.py full $out/${tag}_$r.ncu-rep > $out/${tag}_$r.md 2>&1
+  ncu -i $out/${tag}_$r.ncu-rep --page raw --csv > $out/${tag}_$r.raw.csv 2>/dev/null
+done
+python tools/ncu_summary.py traffic $out/${tag}_prof.ncu-rep c2 > $out/${tag}_traffic_c2.json 2>&1
+python tools/ncu_summary.py traffic $out/${tag}_prof_c4.ncu-rep c4 > $out/${tag}_traffic_c4.json 2>&1
+rm -f $out/${tag}_prof_dense.ncu-rep $out/${tag}_prof_c4.ncu-rep
+gzip -f $out/${tag}_launches.csv $out/${tag}_*.raw.csv
