@@ -346,6 +346,40 @@ def run_ours(args):
     h_loc = layer.table_range[1] - layer.table_range[0]
     G = gathered_bytes_per_token(cfg, elem) * n * h_loc // cfg.tables  # this rank's tables
 
+    # c5 (skewed / small-batch stress): per-call latency at the BASELINE's
+    # small token counts, device time (CUDA events) with the tables warm in
+    # L2 and after an L2 flush, and through the host path
+    small = None
+    if args.config == "c5" and mode == "token":
+        small = {}
+        for m in (1, 8, 64):
+            res = {}
+            for cold in (False, True):
+                ts = []
+                for r in range(60):
+                    if cold:
+                        flush.fill_(r & 0xFF)
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    layer.forward_device(xd[:m], yd[:m], stream=stream)
+                    e1.record(stream)
+                    torch.cuda.synchronize()
+                    if r >= 10:
+                        ts.append(e0.elapsed_time(e1) * 1e3)
+                res["device_us_cold_l2" if cold else "device_us_warm_l2"] = round(
+                    float(np.median(ts)), 2)
+            hxm = torch.from_numpy(np.ascontiguousarray(x[:m])).pin_memory()
+            hym = torch.empty((m, cfg.d_out), dtype=torch.float32).pin_memory()
+            ts = []
+            for r in range(60):
+                t0 = time.perf_counter()
+                layer.forward_host_ptr(hxm.data_ptr(), m, hym.data_ptr())
+                if r >= 10:
+                    ts.append((time.perf_counter() - t0) * 1e6)
+            res["host_path_us"] = round(float(np.median(ts)), 2)
+            small[str(m)] = res
+
     # end-to-end through the C-ABI host path: pinned host x -> y
     hx = torch.from_numpy(x).pin_memory()
     hy = torch.empty((n, cfg.d_out), dtype=torch.float32).pin_memory()
@@ -449,6 +483,8 @@ def run_ours(args):
                                       "other": fl.other_mflop},
             "clocks": clocks.summary(),
         }
+        if small is not None:
+            result["small_batch_latency"] = small
     if dist:
         dist.barrier()
         dist.destroy_process_group()

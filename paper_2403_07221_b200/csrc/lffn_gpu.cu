@@ -9,6 +9,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <mutex>
+#include <unordered_map>
 #include <cstdint>
 #include <cstring>
 #include <string>
@@ -39,6 +41,23 @@ int fail(int status, const std::string& msg) {
 }  // namespace lffn_gpu
 
 using namespace lffn_gpu;
+
+namespace {
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and size:
+// a host API call per launch is measurable at small batches
+void set_smem(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::unordered_map<uint64_t, int> done;  // (kernel, device) -> bytes set
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t key = reinterpret_cast<uintptr_t>(fn) * 64u + uint64_t(dev);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = done.find(key);
+  if (it != done.end() && it->second >= bytes) return;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  done[key] = bytes;
+}
+}  // namespace
 
 #define LFFN_CUDA(call)                                                                   \
   do {                                                                                    \
@@ -362,7 +381,7 @@ int launch_hash_top1(lffn_ctx* c, const float* d_x, int64_t n, uint32_t* codes, 
     const size_t smem = size_t(p.tokens_per_block) * size_t(padded_len(int(c->D))) * sizeof(double);
     const unsigned grid = (unsigned)((n + p.tokens_per_block - 1) / p.tokens_per_block);
     auto gob = [&](auto kernel) {
-      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      set_smem(reinterpret_cast<const void*>(kernel), int(smem));
       kernel<<<grid, 512, smem, st>>>(p, bh);
     };
     switch (loge5) {
@@ -473,7 +492,7 @@ int launch_hash_top1(lffn_ctx* c, const float* d_x, int64_t n, uint32_t* codes, 
                    : c->proj.kind == LFFN_PROJ_ACDC   ? kPreDiag
                                                       : kPreNone;
   auto go = [&](auto kernel) {
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    set_smem(reinterpret_cast<const void*>(kernel), int(smem));
     kernel<<<grid, block, smem, st>>>(p);
   };
   // the pair kernel is exact but measured slower (shuffle traffic throttles
@@ -485,7 +504,7 @@ int launch_hash_top1(lffn_ctx* c, const float* d_x, int64_t n, uint32_t* codes, 
     const size_t smem2 = size_t(tpb2) * size_t(pair_padded_len(int(c->D))) * sizeof(double);
     const unsigned grid2 = (unsigned)((n + tpb2 - 1) / tpb2);
     auto go2 = [&](auto kernel) {
-      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2));
+      set_smem(reinterpret_cast<const void*>(kernel), int(smem2));
       kernel<<<grid2, 128, smem2, st>>>(p);
     };
     if (c->logD == 11) {
@@ -773,7 +792,7 @@ int launch_fused(lffn_ctx* c, const FusedChoice& f, const float* d_x, int64_t n,
   } else {
     return fail(LFFN_ERR_USAGE, "fused forward: no kernel for this shape");
   }
-  LFFN_CUDA(cudaFuncSetAttribute(f.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  set_smem(reinterpret_cast<const void*>(f.fn), int(smem));
   f.fn<<<grid, f.block, smem, st>>>(fp);
   ++c->launches;
   LFFN_CUDA(cudaGetLastError());
@@ -1250,7 +1269,7 @@ int launch_rows_fwht(lffn_ctx* c, double* V, int64_t n, cudaStream_t st) {
   const size_t smem = size_t(tpb) * size_t(padded_len(int(c->D))) * sizeof(double);
   const unsigned grid = unsigned((n + tpb - 1) / tpb);
   auto go = [&](auto kernel) {
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    set_smem(reinterpret_cast<const void*>(kernel), int(smem));
     kernel<<<grid, block, smem, st>>>(p, V);
   };
   switch (loge) {
@@ -1391,7 +1410,7 @@ int launch_proj_backward(lffn_ctx* c, const float* d_x, const double* gz, int64_
   const size_t smem = size_t(tpb) * size_t(padded_len(int(c->D))) * sizeof(double);
   const unsigned grid = unsigned((n + tpb - 1) / tpb);
   auto go = [&](auto kernel) {
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    set_smem(reinterpret_cast<const void*>(kernel), int(smem));
     kernel<<<grid, block, smem, st>>>(p, gz, c->d_signmask, d_grad_x);
   };
   switch (loge) {
