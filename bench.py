@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--tokens", type=int, default=0, help="override the batch size")
     ap.add_argument("--cpu-sample", type=int, default=0, help="reference-arm tokens per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--hash-mode", default="token", choices=["token", "replicated"],
+                    help="table sharding: hash the rank's own token block and all-to-all the "
+                         "records (token), or recompute the full hash on every rank")
     ap.add_argument("--shard", default="auto", choices=["auto", "token", "table"],
                     help="N>1 partitioning: token (tables replicated, c1/c2/c5) or table "
                          "(tables split over ranks, partials combined by NCCL; c3/c4); "
@@ -275,6 +278,7 @@ def run_ours(args):
         n = ((n + q - 1) // q) * q
         x = make_x(w, n, seed=0)
         sharded = ShardedLookupFFN(cfg, proj, T, mode="table", combine=combine, device=local,
+                                   hash_mode=args.hash_mode,
                                    max_tokens=n, table_dtype=w.table_dtype, chunks=chunks)
         layer = sharded.layer
     del T
@@ -441,7 +445,9 @@ def run_ours(args):
                 "parallelism": (f"token-sharded x{world} (tables replicated)" if mode == "token"
                                 else f"table-sharded x{world} (tables [{layer.table_range[0]}, "
                                      f"{layer.table_range[1]}) on rank 0; NCCL {combine} of the "
-                                     f"fp32 partials, 4 chunks overlapped)"),
+                                     f"fp32 partials, 4 chunks overlapped; hash "
+                                     + ("of the rank's token block, records all-to-all"
+                                        if args.hash_mode == "token" else "replicated") + ")"),
                 "l2": "flushed before every timed step (256 MiB write outside the events)",
             },
             "e2e": {

@@ -5,12 +5,19 @@ the partitioning follows SURVEY.md 8e / BASELINE.json north_star:
 
 * ``mode="token"``  tables replicated, rank r runs its own token block; no
   collective on the data path (optionally an all-gather of y).
-* ``mode="table"``  rank r owns the table slice [r*h/P, (r+1)*h/P) (the hash
-  is recomputed per rank -- it is cheap -- but codes/coefficients are emitted
-  only for the owned tables, lffn_ctx_create_shard), produces the fp32
-  PARTIAL y over its tables for all tokens, and the partials are combined by
-  ``combine="reduce_scatter"`` (rank r keeps token rows [r*n/P, (r+1)*n/P),
-  BASELINE c3) or ``combine="all_reduce"`` (every rank keeps all of y, c4).
+* ``mode="table"``  rank r owns the table slice [r*h/P, (r+1)*h/P), produces
+  the fp32 PARTIAL y over its tables for all tokens, and the partials are
+  combined by ``combine="reduce_scatter"`` (rank r keeps token rows
+  [r*n/P, (r+1)*n/P), BASELINE c3) or ``combine="all_reduce"`` (every rank
+  keeps all of y, c4).  The hash of a token needs its whole projection (the
+  signflip FWHT mixes every coordinate), so it is not table-separable:
+  ``hash_mode="token"`` (default) hashes only the rank's own token block for
+  ALL tables and exchanges the (code, coeff) records with one all-to-all
+  (rank q receives the records of its tables for every token: n * h/P * 8
+  bytes, against the n * d_out * 4-byte partials of the combine), so the
+  hash costs 1/P per rank; ``hash_mode="replicated"`` recomputes the full
+  hash for all tokens on every rank and keeps only the owned tables'
+  records (lffn_ctx_create_shard).
 
 The combine is pipelined with the compute: tokens are processed in
 ``chunks``; chunk c's collective is issued asynchronously (NCCL runs it on its
@@ -32,6 +39,8 @@ import torch.distributed as dist
 from .lookup import HashTables, LookupConfig, LookupFFN, Projection
 
 PartialFn = Callable[[torch.Tensor, torch.Tensor], None]
+HashFn = Callable[[torch.Tensor], Tuple[torch.Tensor, torch.Tensor]]
+GatherFn = Callable[[torch.Tensor, torch.Tensor, torch.Tensor], None]
 
 
 def split_range(total: int, parts: int, index: int) -> Tuple[int, int]:
@@ -45,13 +54,17 @@ class ShardedLookupFFN:
     def __init__(self, cfg: LookupConfig, proj: Projection, tables: Optional[HashTables], *,
                  mode: str = "table", combine: str = "reduce_scatter", group=None,
                  device: Optional[int] = None, max_tokens: int = 65536,
-                 table_dtype: str = "f32", chunks: int = 4,
-                 partial_fn: Optional[PartialFn] = None):
+                 table_dtype: str = "f32", chunks: int = 4, hash_mode: str = "token",
+                 partial_fn: Optional[PartialFn] = None, hash_fn: Optional[HashFn] = None,
+                 gather_fn: Optional[GatherFn] = None):
         if mode not in ("table", "token"):
             raise ValueError(f"unknown mode {mode}")
         if combine not in ("reduce_scatter", "all_reduce", "none"):
             raise ValueError(f"unknown combine {combine}")
+        if hash_mode not in ("token", "replicated"):
+            raise ValueError(f"unknown hash_mode {hash_mode}")
         self.cfg, self.mode, self.combine = cfg, mode, combine
+        self.hash_mode = hash_mode if mode == "table" else "replicated"
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
@@ -61,7 +74,8 @@ class ShardedLookupFFN:
         else:
             self.table_range = (0, cfg.tables)
         self.layer = None
-        if partial_fn is None:
+        self.hasher = None
+        if partial_fn is None and (self.hash_mode == "replicated" or gather_fn is None):
             dev = torch.cuda.current_device() if device is None else device
             self.layer = LookupFFN(cfg, proj, tables, device=dev, max_tokens=max_tokens,
                                    table_dtype=table_dtype, table_range=self.table_range)
@@ -69,7 +83,21 @@ class ShardedLookupFFN:
             def partial_fn(x, out):
                 self.layer.forward_device(x, out)
 
+            def gather_fn(codes, coeff, out):
+                self.layer.lookup_accumulate(codes, coeff, out)
+
+            if self.hash_mode == "token" and hash_fn is None:
+                # all tables, this rank's token block only (no tables needed)
+                per = (max_tokens + self.world - 1) // self.world
+                self.hasher = LookupFFN(cfg, proj, None, device=dev, max_tokens=max(1, per),
+                                        table_range=(0, cfg.tables))
+
+                def hash_fn(x):
+                    return self.hasher.hash(x)
+
         self.partial_fn = partial_fn
+        self.hash_fn = hash_fn
+        self.gather_fn = gather_fn
 
     # ------------------------------------------------------------------
     def rows_owned(self, n: int) -> Tuple[int, int]:
@@ -90,15 +118,44 @@ class ShardedLookupFFN:
             self.partial_fn(x, y)
             return y
         n = x.shape[0]
+        if self.hash_mode == "token":
+            codes, coeff = self.exchange_records(x)
+            part = _RowGather(self.gather_fn, codes, coeff)
+        else:
+            part = _PartialFromX(self.partial_fn)
         if self.combine == "all_reduce":
-            return self._table_all_reduce(x, out)
+            return self._table_all_reduce(x, out, part)
         if self.combine == "none":
             y = out if out is not None else x.new_empty((n, self.cfg.d_out))
-            self.partial_fn(x, y)
+            part(x, y, slice(0, n))
             return y
-        return self._table_reduce_scatter(x, out)
+        return self._table_reduce_scatter(x, out, part)
 
-    def _table_all_reduce(self, x, out):
+    def exchange_records(self, x: torch.Tensor) -> Tuple[torch.Tensor, torch.Tensor]:
+        """hash_mode="token": hash this rank's token block (split_range of the
+        n rows) for all tables, then one all-to-all so every rank holds the
+        (code, coeff) records of ITS tables for all n tokens, token-major
+        ([n, h_r] int32 codes / float32 coefficients, the layout
+        lffn_lookup_accumulate reads)."""
+        n, P, r = x.shape[0], self.world, self.rank
+        h = self.cfg.tables
+        t0, t1 = split_range(n, P, r)
+        codes, coeff = self.hash_fn(x[t0:t1])                      # [m, h] each
+        m = t1 - t0
+        rec = torch.stack([codes.view(torch.int32), coeff.view(torch.int32)], dim=-1)  # [m, h, 2]
+        tranges = [split_range(h, P, q) for q in range(P)]
+        send = torch.cat([rec[:, a:b].reshape(-1) for a, b in tranges]) if m else rec.new_empty(0)
+        kb, ke = self.table_range
+        hl = ke - kb
+        sizes_out = [(split_range(n, P, q)[1] - split_range(n, P, q)[0]) * hl * 2 for q in range(P)]
+        recv = rec.new_empty(sum(sizes_out))
+        dist.all_to_all_single(recv, send, output_split_sizes=sizes_out,
+                               input_split_sizes=[m * (b - a) * 2 for a, b in tranges],
+                               group=self.group)
+        recv = recv.view(n, hl, 2)
+        return (recv[..., 0].contiguous(), recv[..., 1].contiguous().view(torch.float32))
+
+    def _table_all_reduce(self, x, out, part):
         n, d = x.shape[0], self.cfg.d_out
         y = out if out is not None else x.new_empty((n, d))
         works = []
@@ -106,14 +163,14 @@ class ShardedLookupFFN:
             r0, r1 = split_range(n, self.chunks, c)
             if r0 == r1:
                 continue
-            self.partial_fn(x[r0:r1], y[r0:r1])
+            part(x[r0:r1], y[r0:r1], slice(r0, r1))
             works.append(dist.all_reduce(y[r0:r1], op=dist.ReduceOp.SUM, group=self.group,
                                          async_op=True))
         for w in works:
             w.wait()
         return y
 
-    def _table_reduce_scatter(self, x, out):
+    def _table_reduce_scatter(self, x, out, part):
         n, d = x.shape[0], self.cfg.d_out
         P, C = self.world, self.chunks
         if n % (P * C) != 0:
@@ -130,7 +187,7 @@ class ShardedLookupFFN:
                 works[-len(bufs)].wait()  # buffer reuse after its collective
             for r in range(P):
                 rows = slice(r * per_rank + c * sub, r * per_rank + (c + 1) * sub)
-                self.partial_fn(x[rows], buf[r * sub:(r + 1) * sub])
+                part(x[rows], buf[r * sub:(r + 1) * sub], rows)
             works.append(dist.reduce_scatter_tensor(y[c * sub:(c + 1) * sub], buf,
                                                     op=dist.ReduceOp.SUM, group=self.group,
                                                     async_op=True))
@@ -141,3 +198,27 @@ class ShardedLookupFFN:
     def close(self):
         if self.layer is not None:
             self.layer.close()
+        if self.hasher is not None:
+            self.hasher.close()
+
+
+class _PartialFromX:
+    """part(x_rows, out, rows) for hash_mode="replicated": the full forward of
+    the rows over the rank's tables."""
+
+    def __init__(self, fn):
+        self.fn = fn
+
+    def __call__(self, xr, out, rows=None):
+        self.fn(xr, out)
+
+
+class _RowGather:
+    """part(x_rows, out, rows) for hash_mode="token": the gather of the rows'
+    exchanged records over the rank's tables."""
+
+    def __init__(self, fn, codes, coeff):
+        self.fn, self.codes, self.coeff = fn, codes, coeff
+
+    def __call__(self, xr, out, rows):
+        self.fn(self.codes[rows], self.coeff[rows], out)

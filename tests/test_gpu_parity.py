@@ -378,9 +378,10 @@ def test_table_sharded_world1_nccl_path(oracle):
     dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
                             device_id=torch.device("cuda", 0))
     try:
-        for combine in ("reduce_scatter", "all_reduce"):
+        for combine, hash_mode in [(c, hm) for c in ("reduce_scatter", "all_reduce")
+                                   for hm in ("token", "replicated")]:
             sh = ShardedLookupFFN(cfg, proj, T, mode="table", combine=combine, device=0,
-                                  max_tokens=64, chunks=4)
+                                  max_tokens=64, chunks=4, hash_mode=hash_mode)
             y = sh.forward(torch.from_numpy(x).cuda())
             torch.cuda.synchronize()
             np.testing.assert_array_equal(y.cpu().numpy(), plain)

@@ -33,7 +33,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, mode, combine, chunks, result_q):
+def _worker(rank, world, port, mode, combine, chunks, result_q, hash_mode="replicated"):
     import sys
 
     sys.path.insert(0, ROOT)
@@ -65,8 +65,28 @@ def _worker(rank, world, port, mode, combine, chunks, result_q):
             part = orc.gather(T.reshape(h, -1)[kb:ke].ravel(), ke - kb, 16, d, codes, w)
             out.copy_(torch.from_numpy(part.astype(np.float32)))
 
-        m = ShardedLookupFFN(cfg, proj, None, mode=mode, combine=combine, chunks=chunks,
-                             partial_fn=partial_fn)
+        hashed = []
+
+        def hash_fn(xr):
+            # all tables' records of the rank's own token block
+            hashed.append(xr.shape[0])
+            _, cache = orc.lookup_forward(c, s, blob, T, xr.numpy().astype(np.float64), True)
+            codes = np.ascontiguousarray(cache["codes"][:, :, 0]).astype(np.int32)
+            w = np.ascontiguousarray(cache["weights"][:, :, 0]).astype(np.float32)
+            return torch.from_numpy(codes), torch.from_numpy(w)
+
+        def gather_fn(codes, w, out):
+            kb, ke = holder["m"].table_range
+            part = orc.gather(T.reshape(h, -1)[kb:ke].ravel(), ke - kb, 16, d,
+                              codes.numpy().astype(np.uint32), w.numpy().astype(np.float64))
+            out.copy_(torch.from_numpy(part.astype(np.float32)))
+
+        if hash_mode == "token":
+            m = ShardedLookupFFN(cfg, proj, None, mode=mode, combine=combine, chunks=chunks,
+                                 hash_mode="token", hash_fn=hash_fn, gather_fn=gather_fn)
+        else:
+            m = ShardedLookupFFN(cfg, proj, None, mode=mode, combine=combine, chunks=chunks,
+                                 hash_mode="replicated", partial_fn=partial_fn)
         holder["m"] = m
         if mode == "token":
             r0, r1 = split_range(n, world, rank)
@@ -75,26 +95,42 @@ def _worker(rank, world, port, mode, combine, chunks, result_q):
         elif combine == "all_reduce":
             y = m.forward(torch.from_numpy(x))
             expect = y_full
+        elif combine == "none":
+            # the rank's partial sum over its tables, all tokens
+            y = m.forward(torch.from_numpy(x))
+            kb, ke = m.table_range
+            _, cache = orc.lookup_forward(c, s, blob, T, x.astype(np.float64), True)
+            expect = orc.gather(T.reshape(h, -1)[kb:ke].ravel(), ke - kb, 16, d,
+                                np.ascontiguousarray(cache["codes"][:, kb:ke, 0]),
+                                np.ascontiguousarray(cache["weights"][:, kb:ke, 0]))
         else:
             y = m.forward(torch.from_numpy(x))
             r0, r1 = m.rows_owned(n)
             expect = y_full[r0:r1]
         err = float(np.max(np.abs(y.numpy() - expect)) / np.max(np.abs(expect)))
+        if hash_mode == "token":
+            # each rank hashed only its own token block, once
+            assert hashed == [split_range(n, world, rank)[1] - split_range(n, world, rank)[0]]
         result_q.put((rank, m.table_range, tuple(y.shape), err))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode,combine,chunks", [("table", "reduce_scatter", 1),
-                                                 ("table", "reduce_scatter", 3),
-                                                 ("table", "all_reduce", 2),
-                                                 ("token", "none", 1)])
-def test_sharded_two_ranks(mode, combine, chunks):
+@pytest.mark.parametrize("mode,combine,chunks,hash_mode", [
+    ("table", "reduce_scatter", 1, "replicated"),
+    ("table", "reduce_scatter", 3, "replicated"),
+    ("table", "all_reduce", 2, "replicated"),
+    ("token", "none", 1, "replicated"),
+    ("table", "reduce_scatter", 1, "token"),
+    ("table", "reduce_scatter", 3, "token"),
+    ("table", "all_reduce", 2, "token"),
+    ("table", "none", 1, "token")])
+def test_sharded_two_ranks(mode, combine, chunks, hash_mode):
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, combine, chunks, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, combine, chunks, q, hash_mode))
              for r in range(world)]
     for p in procs:
         p.start()
