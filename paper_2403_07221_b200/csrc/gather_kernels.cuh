@@ -425,13 +425,16 @@ __global__ void __launch_bounds__(256, MINB) gather_row_persistent_kernel(Gather
     for (int c = 0; c < MAXC; ++c) {
       if (!ok[c]) continue;
       const int col = colbase + c * CHUNK;
+      if (p.accumulate) {
 #pragma unroll
-      for (int v = 0; v < VEC; ++v) {
-        float o = acc[c][v];
-        if (p.accumulate) o += yr[col + v];
-        if (!isfinite(o)) bad = 4;
-        acc[c][v] = o;
+        for (int v = 0; v < VEC; v += 4) {
+          const float4 a = *reinterpret_cast<const float4*>(yr + col + v);
+          acc[c][v] += a.x; acc[c][v + 1] += a.y; acc[c][v + 2] += a.z; acc[c][v + 3] += a.w;
+        }
       }
+#pragma unroll
+      for (int v = 0; v < VEC; ++v)
+        if (!isfinite(acc[c][v])) bad = 4;
 #pragma unroll
       for (int v = 0; v < VEC; v += 4)
         *reinterpret_cast<float4*>(yr + col + v) =
