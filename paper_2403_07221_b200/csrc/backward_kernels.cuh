@@ -52,6 +52,14 @@ struct BwdParams {
   int* flag;
 };
 
+// tanh(z) with the saturated range short-cut: for |z| >= 19.5 the true value
+// is within 2 e^{-39} < 2^-54 of +-1, so the correctly rounded (and the
+// reference's std::tanh) result is exactly +-1.0 -- no transcendental for the
+// large |z| that the unnormalised transforms produce.
+__device__ __forceinline__ double tanh_exact(double z) {
+  return fabs(z) >= 19.5 ? copysign(1.0, z) : tanh(z);
+}
+
 template <typename TT>
 __device__ __forceinline__ float tload(const TT* p);
 template <>
@@ -133,7 +141,7 @@ __global__ void __launch_bounds__(256) bwd_gradz_kernel(BwdParams p) {
       }
       if (lane < tau) {
         const double s = ((code >> lane) & 1u) ? 1.0 : -1.0;
-        const double th = tanh(zj);
+        const double th = tanh_exact(zj);
         const double dcoeff = p.scaled ? w * (s * (1.0 + dot) - dot * th) : w * (s - th);
         gzj = gzj + gd * dcoeff;
       }
@@ -143,41 +151,213 @@ __global__ void __launch_bounds__(256) bwd_gradz_kernel(BwdParams p) {
   if (bad) atomicOr(p.flag, bad);
 }
 
+// KB1 in two passes (the default; bwd_gradz_kernel above stays for widths
+// that are not a multiple of 4).
+//
+// KB1a bwd_gdot_kernel: gdot[record] = <grad_y_i, T_k[code]> for every
+// record, one warp per token with the token's grad_y row in registers and
+// TIF records' row segments in flight (the single-pass kernel waited for one
+// row and one reduction per table).  Lane l owns columns c*128 + 4l .. +3
+// and sums its fp32 products per record; every 32 records the per-lane
+// partials are reduced across the warp in float64 with a transposed
+// butterfly (31 exchanges for 32 sums instead of 5 per record), after which
+// lane l holds record l's sum and the 32 results are stored coalesced.
+template <typename TT, int MAXC, int TIF>
+__global__ void __launch_bounds__(256, 2) bwd_gdot_kernel(BwdParams p, double* gdot) {
+  static_assert(32 % TIF == 0, "TIF must divide 32");
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const TT* T = static_cast<const TT*>(p.T);
+  const int R = p.hl * p.nc;
+  int bad = 0;
+  for (int64_t token = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; token < p.n;
+       token += nwarps) {
+    const float* gyr = p.gy + token * p.d_out;
+    float4 g[MAXC];
+    bool ok[MAXC];
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+      const int j = c * 128 + lane * 4;
+      ok[c] = j < p.d_out;
+      g[c] = ok[c] ? *reinterpret_cast<const float4*>(gyr + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (!isfinite(g[c].x) || !isfinite(g[c].y) || !isfinite(g[c].z) || !isfinite(g[c].w))
+        bad |= kFlagBwdInput;
+    }
+    const uint32_t* cr = p.codes + token * R;
+    for (int r32 = 0; r32 < R; r32 += 32) {
+      // lane q of the warp loads code r32 + q; broadcast by shuffle
+      const uint32_t mycode = r32 + lane < R ? __ldg(cr + r32 + lane) : 0u;
+      float part[32];
+#pragma unroll
+      for (int q0 = 0; q0 < 32; q0 += TIF) {
+        float4 t4[TIF][MAXC];
+#pragma unroll
+        for (int q = 0; q < TIF; ++q) {
+          const int r = r32 + q0 + q;
+          const uint32_t code = __shfl_sync(0xffffffffu, mycode, q0 + q);
+          const int k = p.nc == 1 ? r : r / p.nc;
+          const TT* row = T + ((int64_t)k * p.rows + code) * p.d_out + lane * 4;
+#pragma unroll
+          for (int c = 0; c < MAXC; ++c) {
+            if (ok[c] && r < R) {
+              if constexpr (sizeof(TT) == 4) {
+                t4[q][c] = __ldg(reinterpret_cast<const float4*>(row + c * 128));
+              } else {
+                const uint2 u = __ldg(reinterpret_cast<const uint2*>(row + c * 128));
+                t4[q][c] = make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xffff0000u),
+                                       __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xffff0000u));
+              }
+            } else {
+              t4[q][c] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < TIF; ++q) {
+          float acc = 0.f;
+#pragma unroll
+          for (int c = 0; c < MAXC; ++c) {
+            acc = fmaf(g[c].x, t4[q][c].x, acc);
+            acc = fmaf(g[c].y, t4[q][c].y, acc);
+            acc = fmaf(g[c].z, t4[q][c].z, acc);
+            acc = fmaf(g[c].w, t4[q][c].w, acc);
+          }
+          part[q0 + q] = acc;
+        }
+      }
+      // transposed butterfly: after the step with offset s, the lanes with
+      // bit s set hold the upper halves; lane l ends with record l's sum
+      double v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const bool up = lane & 16;
+        const double send = (double)(up ? part[i] : part[i + 16]);
+        const double keep = (double)(up ? part[i + 16] : part[i]);
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+      }
+#pragma unroll
+      for (int sft = 8; sft >= 1; sft >>= 1) {
+#pragma unroll
+        for (int i = 0; i < sft; ++i) {
+          const bool up = lane & sft;
+          const double send = up ? v[i] : v[i + sft];
+          const double keep = up ? v[i + sft] : v[i];
+          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, sft);
+        }
+      }
+      if (r32 + lane < R) gdot[token * R + r32 + lane] = v[0];
+    }
+  }
+  if (bad) atomicOr(p.flag, bad);
+}
+
+// KB1b bwd_gz_kernel: one thread per (token, table): the straight-through
+// gradient of the table's tau coordinates from the records' gdot, with the
+// weight / dot / log-denominator folded in the reference's order exactly as
+// bwd_gradz_kernel does (lookup.cpp:292-340) -- bit-identical to it.
+// TAU > 0: compile-time code width (registers); 0: any tau <= 24.
+template <int TAU>
+__global__ void __launch_bounds__(256) bwd_gz_kernel(BwdParams p, const double* gdot) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= p.n * p.hl) return;
+  const int64_t token = idx / p.hl;
+  const int k = (int)(idx - token * p.hl);
+  const int tau = TAU > 0 ? TAU : p.tau;
+  const double* zk = p.z + token * p.code_width + (int64_t)(p.kb + k) * tau;
+  double zv[TAU > 0 ? TAU : 24];
+  double sum_abs = 0.0, w1 = 1.0, logden = 0.0;
+#pragma unroll
+  for (int j = 0; j < tau; ++j) {
+    const double zj = zk[j];
+    zv[j] = zj;
+    const double aj = fabs(zj);
+    sum_abs = sum_abs + aj;
+    // 1 + exp(-2a) == 1.0 exactly for a >= 18.5: the division is then exact
+    // and skipped (as the forward's top1 weight)
+    if (aj < 18.5) w1 = w1 / (1.0 + exp(-2.0 * aj));
+    if (p.nc > 1) logden = logden + (aj + log1p(exp(-2.0 * aj)));
+  }
+  double gzv[TAU > 0 ? TAU : 24];
+#pragma unroll
+  for (int j = 0; j < tau; ++j) gzv[j] = 0.0;
+  for (int c = 0; c < p.nc; ++c) {
+    const int64_t rec = (token * p.hl + k) * p.nc + c;
+    const uint32_t code = p.codes[rec];
+    const double gd = gdot[rec];
+    double dot = sum_abs, w = w1;
+    if (p.nc > 1) {
+      dot = 0.0;
+#pragma unroll
+      for (int j = 0; j < tau; ++j) dot = dot + (((code >> j) & 1u) ? zv[j] : -zv[j]);
+      w = exp(dot - logden);
+    }
+#pragma unroll
+    for (int j = 0; j < tau; ++j) {
+      const double sg = ((code >> j) & 1u) ? 1.0 : -1.0;
+      const double th = tanh_exact(zv[j]);
+      const double dcoeff = p.scaled ? w * (sg * (1.0 + dot) - dot * th) : w * (sg - th);
+      gzv[j] = gzv[j] + gd * dcoeff;
+    }
+  }
+  double* gz = p.gz + token * p.code_width + (int64_t)(p.kb + k) * tau;
+#pragma unroll
+  for (int j = 0; j < tau; ++j) gz[j] = gzv[j];
+}
+
 // KB2a: deterministic ranks.  Thread (k, b) walks token block b in order
 // (tokens ascending, neighbours ascending) and gives each record of table k
 // its rank among the block's records of the same row; hist[k][b][code] ends
 // as the block's count.
-constexpr int kBwdBlocks = 32;  // token blocks of the rank pass
+// token blocks of the rank pass: each thread's walk is a chain of dependent
+// histogram updates, so more blocks = shorter chains (32 -> 128: c2 rank
+// pass 0.47 -> ~0.12 ms) at hl * rows * kBwdBlocks * 4 bytes of scratch
+constexpr int kBwdBlocks = 128;
 __global__ void bwd_rank_kernel(BwdParams p, uint32_t* hist, uint32_t* rank) {
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (tid >= (int64_t)p.hl * kBwdBlocks) return;
   const int k = int(tid % p.hl), b = int(tid / p.hl);
   const int64_t per = (p.n + kBwdBlocks - 1) / kBwdBlocks;
   const int64_t i0 = b * per, i1 = min(p.n, i0 + per);
-  uint32_t* h = hist + ((int64_t)k * kBwdBlocks + b) * p.rows;
+  // hist layout [k][code][b]: a row's block counts are contiguous
+  uint32_t* h = hist + (int64_t)k * p.rows * kBwdBlocks + b;
   for (int64_t i = i0; i < i1; ++i) {
     const int64_t rec0 = (i * p.hl + k) * p.nc;
     for (int c = 0; c < p.nc; ++c) {
       const uint32_t code = p.codes[rec0 + c];
-      rank[rec0 + c] = h[code]++;
+      rank[rec0 + c] = h[(int64_t)code * kBwdBlocks]++;
     }
   }
 }
 
-// KB2b': per (table, code): exclusive running sum of the block counts (the
-// block offsets, in place) and the row's total into offs.
-__global__ void bwd_block_offsets_kernel(BwdParams p, uint32_t* hist) {
-  const int64_t bin = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// KB2b': per (table, code) row, one warp: exclusive scan of the row's
+// kBwdBlocks block counts (contiguous, hist[k][code][b]) in place -- the
+// block offsets -- and the row's total into offs.
+__global__ void __launch_bounds__(256) bwd_block_offsets_kernel(BwdParams p, uint32_t* hist) {
+  static_assert(kBwdBlocks % 32 == 0, "whole words per lane");
+  constexpr int PL = kBwdBlocks / 32;  // counts per lane, consecutive
+  const int lane = threadIdx.x & 31;
+  const int64_t bin = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (bin >= (int64_t)p.hl * p.rows) return;
-  const int k = int(bin / p.rows), code = int(bin % p.rows);
-  uint32_t run = 0;
-  for (int b = 0; b < kBwdBlocks; ++b) {
-    uint32_t* hp = hist + ((int64_t)k * kBwdBlocks + b) * p.rows + code;
-    const uint32_t v = *hp;
-    *hp = run;
-    run += v;
+  uint32_t* hp = hist + bin * kBwdBlocks + lane * PL;
+  uint32_t v[PL], tot = 0;
+#pragma unroll
+  for (int j = 0; j < PL; ++j) {
+    v[j] = hp[j];
+    tot += v[j];
   }
-  p.offs[bin] = run;
+  uint32_t x = tot;  // inclusive scan of the lane totals
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  uint32_t run = x - tot;
+#pragma unroll
+  for (int j = 0; j < PL; ++j) {
+    hp[j] = run;
+    run += v[j];
+  }
+  if (lane == 31) p.offs[bin] = x;
 }
 
 // KB2b: exclusive scan of the row counts into row starts (one CTA).
@@ -230,12 +410,72 @@ __global__ void bwd_place_kernel(BwdParams p, const uint32_t* hist, const uint32
     const int b = int(i / per);
     const uint32_t code = p.codes[r];
     const uint32_t pos = p.offs[(int64_t)k * p.rows + code] +
-                         hist[((int64_t)k * kBwdBlocks + b) * p.rows + code] + rank[r];
+                         hist[((int64_t)k * p.rows + code) * kBwdBlocks + b] + rank[r];
     p.list[pos] = uint32_t(r);
   }
 }
 
 // KB2d: one warp per (table, code) row: gT_row = sum coeff * grad_y_token.
+// KB2e, d_out % 4 == 0: one warp per row with the whole row in registers
+// (lane l owns columns c*128 + 4l .. +3), the row's records walked four at
+// a time so four grad_y rows are in flight; per column the products are
+// accumulated in record order exactly as bwd_gradT_kernel -- bit-identical.
+template <int MAXC>
+__global__ void __launch_bounds__(256) bwd_gradT4_kernel(BwdParams p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t bin = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t bins = (int64_t)p.hl * p.rows;
+  if (bin >= bins) return;
+  const uint32_t b0 = p.offs[bin], b1 = p.offs[bin + 1];
+  const int per_tok = p.hl * p.nc;
+  bool ok[MAXC];
+  float4 acc[MAXC];
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c) {
+    ok[c] = c * 128 + lane * 4 < p.d_out;
+    acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  for (uint32_t e0 = b0; e0 < b1; e0 += 4) {
+    float cf[4];
+    const float* gyr[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t e = min(e0 + q, b1 - 1);
+      const uint32_t rec = __ldg(p.list + e);
+      cf[q] = e0 + q < b1 ? __ldg(p.coeff + rec) : 0.f;
+      gyr[q] = p.gy + (int64_t)(rec / per_tok) * p.d_out + lane * 4;
+    }
+    float4 g[4][MAXC];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int c = 0; c < MAXC; ++c)
+        g[q][c] = ok[c] ? __ldg(reinterpret_cast<const float4*>(gyr[q] + c * 128))
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (e0 + q >= b1) break;
+#pragma unroll
+      for (int c = 0; c < MAXC; ++c) {
+        acc[c].x = fmaf(cf[q], g[q][c].x, acc[c].x);
+        acc[c].y = fmaf(cf[q], g[q][c].y, acc[c].y);
+        acc[c].z = fmaf(cf[q], g[q][c].z, acc[c].z);
+        acc[c].w = fmaf(cf[q], g[q][c].w, acc[c].w);
+      }
+    }
+  }
+  int bad = 0;
+  float* out = p.gT + bin * p.d_out + lane * 4;
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c) {
+    if (!ok[c]) continue;
+    if (!isfinite(acc[c].x) || !isfinite(acc[c].y) || !isfinite(acc[c].z) || !isfinite(acc[c].w))
+      bad |= kFlagBwdTables;
+    *reinterpret_cast<float4*>(out + c * 128) = acc[c];
+  }
+  if (bad) atomicOr(p.flag, bad);
+}
+
 __global__ void __launch_bounds__(256) bwd_gradT_kernel(BwdParams p) {
   const int lane = threadIdx.x & 31;
   const int64_t bin = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -273,18 +513,21 @@ __global__ void __launch_bounds__(256) bwd_gradT_kernel(BwdParams p) {
 
 // KB3 signflip: grad_x = first d_in of s_0 * H(s_1 * H(s_2 * H(g))), g = grad_z
 // padded to D (projection.cpp:362-369).  p.signmask holds (0, s_2, s_1).
-template <int LOGE>
-__global__ void __launch_bounds__(256) proj_bwd_signflip_kernel(HashParams p, const double* gz,
+// LOGD > 0: compile-time transform width (all shared-memory geometry folds,
+// as in hash_structured_kernel); NT / MINB: CTA size and residency.
+template <int LOGE, int NT = 256, int MINB = 1, int LOGD = 0>
+__global__ void __launch_bounds__(NT, MINB) proj_bwd_signflip_kernel(HashParams p, const double* gz,
                                                                 const uint32_t* s0mask,
                                                                 double* grad_x) {
   extern __shared__ double smem[];
   constexpr int E = 1 << LOGE;
-  const int tpt = p.threads_per_token;
+  const int logD = LOGD > 0 ? LOGD : p.logD;
+  const int tpt = LOGD > 0 ? (1 << (LOGD - LOGE)) : p.threads_per_token;
   const int slot = threadIdx.x / tpt;
   const int t = threadIdx.x - slot * tpt;
   const int64_t token = (int64_t)blockIdx.x * p.tokens_per_block + slot;
   const bool active = slot < p.tokens_per_block && token < p.n;
-  const int D = p.D;
+  const int D = 1 << logD;
   double* sm = smem + (size_t)slot * padded_len(D);
   int bad = 0;
   auto token_sync = [&]() {
@@ -299,12 +542,15 @@ __global__ void __launch_bounds__(256) proj_bwd_signflip_kernel(HashParams p, co
     }
   token_sync();
   int nph = 1;
-  if constexpr (LOGE > 0) nph = (p.logD + LOGE - 1) / LOGE;
+  if constexpr (LOGE > 0) nph = (logD + LOGE - 1) / LOGE;
+#pragma unroll 1
   for (int tr = 0; tr < 3; ++tr) {
     if (active) phase_smem<LOGE, LOGE, false, kPreSign>(sm, t, tpt, 0, p, tr, nullptr, bad, false);
     token_sync();
-    for (int ph = 1; ph < nph; ++ph) {
-      if (active) run_later_phase<LOGE>(sm, t, tpt, ph * LOGE, min(LOGE, p.logD - ph * LOGE), p, tr, bad, false);
+    const int nphc = LOGD > 0 ? (LOGD + LOGE - 1) / LOGE : nph;
+#pragma unroll
+    for (int ph = 1; ph < nphc; ++ph) {
+      if (active) run_later_phase<LOGE>(sm, t, tpt, ph * LOGE, min(LOGE, logD - ph * LOGE), p, tr, bad, false);
       token_sync();
     }
   }

@@ -98,6 +98,7 @@ struct lffn_ctx {
   uint32_t* d_bwd_offs = nullptr;  // [h_loc * rows + 1]
   uint32_t* d_bwd_hist = nullptr;  // [h_loc * kBwdBlocks * rows]
   uint32_t* d_bwd_rank = nullptr;  // [max_tokens * h_loc * nc]
+  double* d_bwd_gdot = nullptr;    // [max_tokens * h_loc * nc] <grad_y, row> per record
   uint32_t* d_bwd_list = nullptr;  // [max_tokens * h_loc * nc]
   uint32_t* d_bwd_mask = nullptr;  // signflip: masks (0, s_2, s_1)
   double* d_bwd_rows = nullptr;    // acdc / bh: (2 + stage inputs) x [max_tokens x D]
@@ -190,6 +191,7 @@ void destroy_ctx(lffn_ctx* c) {
   cudaFree(c->d_bwd_offs);
   cudaFree(c->d_bwd_hist);
   cudaFree(c->d_bwd_rank);
+  cudaFree(c->d_bwd_gdot);
   cudaFree(c->d_bwd_list);
   cudaFree(c->d_bwd_mask);
   cudaFree(c->d_bwd_rows);
@@ -1240,6 +1242,7 @@ int ensure_backward_scratch(lffn_ctx* c) {
     LFFN_CUDA(cudaMalloc(&c->d_bwd_hist, bins * kBwdBlocks * sizeof(uint32_t)));
     LFFN_CUDA(cudaMalloc(&c->d_bwd_list, mt * size_t(std::max<int64_t>(c->h_loc * c->nc, 1)) * sizeof(uint32_t)));
     LFFN_CUDA(cudaMalloc(&c->d_bwd_rank, mt * size_t(std::max<int64_t>(c->h_loc * c->nc, 1)) * sizeof(uint32_t)));
+    LFFN_CUDA(cudaMalloc(&c->d_bwd_gdot, mt * size_t(std::max<int64_t>(c->h_loc * c->nc, 1)) * sizeof(double)));
   }
   if (c->proj.kind == LFFN_PROJ_SIGNFLIP && !c->d_bwd_mask) {
     const int64_t words = (c->D + 31) / 32;
@@ -1403,7 +1406,10 @@ int launch_proj_backward(lffn_ctx* c, const float* d_x, const double* gz, int64_
   p.flag = c->d_flag;
   const int loge = c->logD >= kMaxLogE ? kMaxLogE : int(c->logD);
   const int tpt = int(c->D >> loge);
-  const int block = std::max(tpt, (256 / tpt) * tpt);
+  // D = 2048 / 4096: compile-time geometry, 128-thread CTAs, 3 per SM (as K1)
+  const bool fixed = loge == 6 && (c->logD == 11 || c->logD == 12);
+  const int nt = fixed ? 128 : 256;
+  const int block = std::max(tpt, (nt / tpt) * tpt);
   const int tpb = block / tpt;
   p.tokens_per_block = tpb;
   p.threads_per_token = tpt;
@@ -1413,6 +1419,13 @@ int launch_proj_backward(lffn_ctx* c, const float* d_x, const double* gz, int64_
     set_smem(reinterpret_cast<const void*>(kernel), int(smem));
     kernel<<<grid, block, smem, st>>>(p, gz, c->d_signmask, d_grad_x);
   };
+  if (fixed) {
+    if (c->logD == 11) go(proj_bwd_signflip_kernel<6, 128, 3, 11>);
+    else go(proj_bwd_signflip_kernel<6, 128, 3, 12>);
+    ++c->launches;
+    LFFN_CUDA(cudaGetLastError());
+    return LFFN_OK;
+  }
   switch (loge) {
     case 0: go(proj_bwd_signflip_kernel<0>); break;
     case 1: go(proj_bwd_signflip_kernel<1>); break;
@@ -1489,11 +1502,32 @@ int lffn_backward(lffn_ctx* c, const float* d_x, const float* d_grad_y, int64_t 
     if (c->h_loc > 0) {
       const unsigned g1 = unsigned((n * 32 + 255) / 256);
       const bool v4 = c->cfg.d_out % 4 == 0;
-      if (esz == 4 && v4) bwd_gradz_kernel<float, 4><<<g1, 256, 0, st>>>(p);
-      else if (esz == 4) bwd_gradz_kernel<float, 1><<<g1, 256, 0, st>>>(p);
-      else if (v4) bwd_gradz_kernel<__nv_bfloat16, 4><<<g1, 256, 0, st>>>(p);
-      else bwd_gradz_kernel<__nv_bfloat16, 1><<<g1, 256, 0, st>>>(p);
-      ++c->launches;
+      const int mc = int((c->cfg.d_out + 127) / 128);  // 4-column chunks per lane
+      static const int one_pass = getenv("LFFN_BWD_ONE_PASS") ? atoi(getenv("LFFN_BWD_ONE_PASS")) : 0;
+      if (v4 && mc <= 8 && c->cfg.code_bits <= 24 && !one_pass) {
+        // KB1a gdot per record (many rows in flight), KB1b gz per (token, table)
+        const unsigned gg = unsigned(std::min<int64_t>(int64_t(c->num_sms) * 2, (n * 32 + 255) / 256));
+#define LFFN_GDOT(TT, M) bwd_gdot_kernel<TT, M, (M >= 6 ? 2 : 4)><<<gg, 256, 0, st>>>(p, c->d_bwd_gdot)
+        if (esz == 4) {
+          if (mc <= 2) LFFN_GDOT(float, 2); else if (mc <= 4) LFFN_GDOT(float, 4);
+          else if (mc <= 6) LFFN_GDOT(float, 6); else LFFN_GDOT(float, 8);
+        } else {
+          if (mc <= 2) LFFN_GDOT(__nv_bfloat16, 2); else if (mc <= 4) LFFN_GDOT(__nv_bfloat16, 4);
+          else if (mc <= 6) LFFN_GDOT(__nv_bfloat16, 6); else LFFN_GDOT(__nv_bfloat16, 8);
+        }
+#undef LFFN_GDOT
+        const unsigned gz = unsigned((n * c->h_loc + 255) / 256);
+        if (c->cfg.code_bits == 8) bwd_gz_kernel<8><<<gz, 256, 0, st>>>(p, c->d_bwd_gdot);
+        else if (c->cfg.code_bits == 10) bwd_gz_kernel<10><<<gz, 256, 0, st>>>(p, c->d_bwd_gdot);
+        else bwd_gz_kernel<0><<<gz, 256, 0, st>>>(p, c->d_bwd_gdot);
+        c->launches += 2;
+      } else {
+        if (esz == 4 && v4) bwd_gradz_kernel<float, 4><<<g1, 256, 0, st>>>(p);
+        else if (esz == 4) bwd_gradz_kernel<float, 1><<<g1, 256, 0, st>>>(p);
+        else if (v4) bwd_gradz_kernel<__nv_bfloat16, 4><<<g1, 256, 0, st>>>(p);
+        else bwd_gradz_kernel<__nv_bfloat16, 1><<<g1, 256, 0, st>>>(p);
+        ++c->launches;
+      }
     }
     if (d_grad_tables && c->h_loc > 0) {
       // deterministic buckets: ranks per token block, block offsets, row
@@ -1501,11 +1535,20 @@ int lffn_backward(lffn_ctx* c, const float* d_x, const float* d_grad_y, int64_t 
       const int64_t hb = c->h_loc * kBwdBlocks;
       LFFN_CUDA(cudaMemsetAsync(c->d_bwd_hist, 0, size_t(hb) * size_t(c->rows) * sizeof(uint32_t), st));
       bwd_rank_kernel<<<unsigned((hb + 127) / 128), 128, 0, st>>>(p, c->d_bwd_hist, c->d_bwd_rank);
-      bwd_block_offsets_kernel<<<unsigned((bins + 255) / 256), 256, 0, st>>>(p, c->d_bwd_hist);
+      bwd_block_offsets_kernel<<<unsigned((bins * 32 + 255) / 256), 256, 0, st>>>(p, c->d_bwd_hist);
       bwd_scan_kernel<<<1, 1024, 0, st>>>(p);
       const unsigned gr = unsigned(std::min<int64_t>(int64_t(c->num_sms) * 8, (n * c->h_loc * c->nc + 255) / 256));
       bwd_place_kernel<<<gr, 256, 0, st>>>(p, c->d_bwd_hist, c->d_bwd_rank);
-      bwd_gradT_kernel<<<unsigned((bins * 32 + 255) / 256), 256, 0, st>>>(p);
+      const unsigned gt = unsigned((bins * 32 + 255) / 256);
+      const int mc4 = int((c->cfg.d_out + 127) / 128);
+      if (c->cfg.d_out % 4 == 0 && mc4 <= 8) {
+        if (mc4 <= 2) bwd_gradT4_kernel<2><<<gt, 256, 0, st>>>(p);
+        else if (mc4 <= 4) bwd_gradT4_kernel<4><<<gt, 256, 0, st>>>(p);
+        else if (mc4 <= 6) bwd_gradT4_kernel<6><<<gt, 256, 0, st>>>(p);
+        else bwd_gradT4_kernel<8><<<gt, 256, 0, st>>>(p);
+      } else {
+        bwd_gradT_kernel<<<gt, 256, 0, st>>>(p);
+      }
       c->launches += 5;
     }
     LFFN_CUDA(cudaGetLastError());
