@@ -1353,7 +1353,7 @@ int launch_proj_backward_stagewise(lffn_ctx* c, const float* d_x, const double* 
       if (d_grad_proj) {
         // grad_B_s[g][r][c] = sum_i src_i[g*b + r] * g_i[g*b + c], tokens ascending
         dim3 grid(unsigned((b + 63) / 64), unsigned((b + 63) / 64), unsigned(D / b));
-        gemm_f64_exact_kernel<double, true, false><<<grid, 256, 0, st>>>(
+        gemm_f64_exact8_kernel<double, true, false><<<grid, 64, 0, st>>>(
             S + size_t(s) * rows, int(D), G, int(D), d_grad_proj + s * stage_size, b, b, b, int(n),
             c->d_flag, b, b, int64_t(b) * b);
         ++c->launches;
@@ -1378,13 +1378,13 @@ int launch_proj_backward(lffn_ctx* c, const float* d_x, const double* gz, int64_
   if (c->proj.kind == LFFN_PROJ_DENSE) {
     if (d_grad_x) {
       dim3 grid(unsigned((d_in + 63) / 64), unsigned((n + 63) / 64));
-      gemm_f64_exact_kernel<double, false, true><<<grid, 256, 0, st>>>(gz, cw, c->d_W, cw, d_grad_x, d_in,
+      gemm_f64_exact8_kernel<double, false, true><<<grid, 64, 0, st>>>(gz, cw, c->d_W, cw, d_grad_x, d_in,
                                                                       int(n), d_in, cw, c->d_flag);
       ++c->launches;
     }
     if (d_grad_proj) {
       dim3 grid(unsigned((cw + 63) / 64), unsigned((d_in + 63) / 64));
-      gemm_f64_exact_kernel<float, true, false><<<grid, 256, 0, st>>>(d_x, d_in, gz, cw, d_grad_proj, cw,
+      gemm_f64_exact8_kernel<float, true, false><<<grid, 64, 0, st>>>(d_x, d_in, gz, cw, d_grad_proj, cw,
                                                                      d_in, cw, int(n), c->d_flag);
       ++c->launches;
     }
