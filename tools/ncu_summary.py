@@ -19,8 +19,14 @@ FULL_METRICS = [
     ("dram__bytes_read.sum", "dram read"),
     ("dram__bytes_write.sum", "dram write"),
     ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "dram % peak"),
-    ("lts__t_bytes.sum", "L2 bytes"),
-    ("lts__t_bytes.sum.per_second", "L2 bytes/s"),
+    ("dram__bytes_read.sum.per_second", "dram read bytes/s"),
+    ("dram__bytes_read.sum.pct_of_peak_sustained_elapsed", "dram read % of peak"),
+    ("l1tex__m_xbar2l1tex_read_bytes.sum.per_second", "L2 -> SM read bytes/s"),
+    ("l1tex__m_xbar2l1tex_read_bytes.sum.pct_of_peak_sustained_elapsed", "L2 -> SM read % of peak"),
+    ("lts__t_sectors.sum.per_second", "L2 sectors/s (x 32 B)"),
+    ("lts__lts2xbar_cycles_active.avg.pct_of_peak_sustained_elapsed", "L2 -> xbar port busy % (avg)"),
+    ("lts__lts2xbar_cycles_active.max.pct_of_peak_sustained_elapsed", "L2 -> xbar port busy % (max slice)"),
+    ("lts__t_sectors_srcunit_ltcfabric.sum.per_second", "L2 sectors/s from the die-to-die fabric"),
     ("lts__t_sector_hit_rate.pct", "L2 hit %"),
     ("l1tex__t_bytes.sum", "L1 bytes"),
     ("l1tex__t_sector_hit_rate.pct", "L1 hit %"),
@@ -65,8 +71,16 @@ def launches(path):
 
 
 def raw(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    """ncu report (.ncu-rep) or its saved raw page (.raw.csv[.gz])."""
+    if path.endswith(".csv") or path.endswith(".csv.gz"):
+        import gzip
+
+        opener = gzip.open if path.endswith(".gz") else open
+        with opener(path, "rt") as f:
+            out = f.read()
+    else:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
     return hdr, units, rows[2:]
