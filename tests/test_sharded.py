@@ -33,7 +33,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, mode, combine, chunks, result_q, hash_mode="replicated"):
+def _worker(rank, world, port, mode, combine, chunks, result_q, hash_mode="replicated", h=10, n=24):
     import sys
 
     sys.path.insert(0, ROOT)
@@ -45,7 +45,7 @@ def _worker(rank, world, port, mode, combine, chunks, result_q, hash_mode="repli
         from paper_2403_07221_b200.sharded import ShardedLookupFFN
 
         orc = Oracle()
-        d, h, tau, n = 32, 10, 4, 24
+        d, tau = 32, 4
         c = Cfg(d, d, h, tau)
         s = Spec(d, h * tau, 3)
         blob = orc.proj_init(s, 1)
@@ -116,21 +116,26 @@ def _worker(rank, world, port, mode, combine, chunks, result_q, hash_mode="repli
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode,combine,chunks,hash_mode", [
-    ("table", "reduce_scatter", 1, "replicated"),
-    ("table", "reduce_scatter", 3, "replicated"),
-    ("table", "all_reduce", 2, "replicated"),
-    ("token", "none", 1, "replicated"),
-    ("table", "reduce_scatter", 1, "token"),
-    ("table", "reduce_scatter", 3, "token"),
-    ("table", "all_reduce", 2, "token"),
-    ("table", "none", 1, "token")])
-def test_sharded_two_ranks(mode, combine, chunks, hash_mode):
+@pytest.mark.parametrize("mode,combine,chunks,hash_mode,h,n", [
+    ("table", "reduce_scatter", 1, "replicated", 10, 24),
+    ("table", "reduce_scatter", 3, "replicated", 10, 24),
+    ("table", "all_reduce", 2, "replicated", 10, 24),
+    ("token", "none", 1, "replicated", 10, 24),
+    ("table", "reduce_scatter", 1, "token", 10, 24),
+    ("table", "reduce_scatter", 3, "token", 10, 24),
+    ("table", "all_reduce", 2, "token", 10, 24),
+    ("table", "none", 1, "token", 10, 24),
+    # uneven table split (6 / 5) and uneven token blocks (13 / 12) for the
+    # all-to-all's split sizes
+    ("table", "all_reduce", 1, "token", 11, 25),
+    ("table", "none", 1, "token", 11, 25)])
+def test_sharded_two_ranks(mode, combine, chunks, hash_mode, h, n):
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, combine, chunks, q, hash_mode))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, combine, chunks, q, hash_mode,
+                                               h, n))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -140,8 +145,8 @@ def test_sharded_two_ranks(mode, combine, chunks, hash_mode):
         assert p.exitcode == 0
     ranges = [r[1] for r in results]
     if mode == "table":
-        assert ranges == [(0, 5), (5, 10)]
+        assert ranges == [(0, (h + 1) // 2), ((h + 1) // 2, h)]
     for rank, _, shape, err in results:
         assert err < 2e-6, (rank, err)
         if mode == "table" and combine == "reduce_scatter":
-            assert shape == (12, 32)
+            assert shape == (n // 2, 32)
