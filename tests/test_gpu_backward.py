@@ -152,3 +152,25 @@ def test_backward_non_finite_grad_y_raises():
     layer.backward(torch.from_numpy(x).cuda(), torch.from_numpy(gy).cuda())
     with pytest.raises(NumericError, match="lookup backward input"):
         layer.sync()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["c2", "c2_bf16"])
+def test_two_pass_kb1_bit_identical_to_one_pass(tmp_path, name):
+    """The default backward (gdot pass with the transposed float64 butterfly,
+    per-(token, table) gz pass, four-row table-gradient walk) against the
+    single-pass KB1 (LFFN_BWD_ONE_PASS=1, read once per process): grad_x and
+    grad_T bit-identical."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    tool = os.path.join(root, "tools", "bwd_ab_check.py")
+    for tag, env in (("a", {"LFFN_BWD_ONE_PASS": "1"}), ("b", {})):
+        subprocess.run([sys.executable, tool, name, str(tmp_path / tag)], check=True,
+                       env={**os.environ, **env}, timeout=600)
+    for suffix in (".npy", "_T.npy"):
+        a = np.load(str(tmp_path / ("a" + suffix)))
+        b = np.load(str(tmp_path / ("b" + suffix)))
+        assert np.array_equal(a, b), suffix

@@ -1,5 +1,11 @@
+"""A/B of the backward paths: grad_x and grad_T of one configuration saved to
+<out>.npy / <out>_T.npy (run once with LFFN_BWD_ONE_PASS=1 and once without,
+then compare the files).
+
+    python tools/bwd_ab_check.py c2 /tmp/a
+"""
 import os, sys
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from paper_2403_07221_b200 import LookupFFN, ProjKind
 from paper_2403_07221_b200.configs import WORKLOADS, make_params, make_x
