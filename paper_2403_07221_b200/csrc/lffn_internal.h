@@ -32,7 +32,7 @@ enum : int {
   kFlagBwdInput = 8,    // "lookup backward input" / "projection backward input"
   kFlagBwdOutput = 16,  // "projection backward output"
   kFlagBwdTables = 32,  // "lookup backward tables"
-  kFlagStream = 64,     // host pipeline: a device-side wait on a copy timed out
+  kFlagStream = 64,     // a bounded device-side wait timed out (fused kernel ring)
 };
 
 }  // namespace lffn_gpu
