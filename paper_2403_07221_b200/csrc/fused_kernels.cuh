@@ -106,8 +106,12 @@ __device__ __forceinline__ bool bar_wait(uint64_t* b, uint32_t parity, int64_t l
 // order the ring.  The gather warps never stop issuing row loads for hash
 // work, and the hash runs in the issue slots the latency-bound gather
 // leaves idle.  Each CTA owns a contiguous token range.
-template <typename TT, int TAU, int MAXC, int HP, int R>
-__global__ void __launch_bounds__(512, 1) fused_ws_kernel(FusedParams fp) {
+// GWT > 0: that many gather warps (else 16 - 2 HP); ANS > 0: the gather warps
+// stage their rows in shared memory (AsyncWalk, ANS stages of one table)
+// instead of registers, which leaves the register file to the hash warps.
+template <typename TT, int TAU, int MAXC, int HP, int R, int GWT = 0, int ANS = 0>
+__global__ void __launch_bounds__(32 * (2 * HP + (GWT > 0 ? GWT : 16 - 2 * HP)), 1)
+    fused_ws_kernel(FusedParams fp) {
   extern __shared__ __align__(16) unsigned char fws_smem[];
   constexpr int LOGE = 5;
   constexpr int E = 1 << LOGE;
@@ -115,7 +119,7 @@ __global__ void __launch_bounds__(512, 1) fused_ws_kernel(FusedParams fp) {
   constexpr int D = 1 << LOGD;
   constexpr int TPT = D / E;            // 64 threads per token
   constexpr int KMAX = E / TAU + 1;
-  constexpr int GW = 16 - 2 * HP;       // gather warps
+  constexpr int GW = GWT > 0 ? GWT : 16 - 2 * HP;  // gather warps
   constexpr int VEC = Raw<TT>::VEC;
   constexpr int CHUNK = 32 * VEC;
   constexpr int TIF = 4;
@@ -208,6 +212,48 @@ __global__ void __launch_bounds__(512, 1) fused_ws_kernel(FusedParams fp) {
     // ---------------- gather warps
     const int gw = warp - 2 * HP;
     const int nchunks = (g.d_out + CHUNK - 1) / CHUNK;
+    if constexpr (ANS > 0) {
+      using Wk = AsyncWalk<TT, MAXC, 1, ANS>;
+      uint4* gring = reinterpret_cast<uint4*>(ring + (size_t)R * rec_slot) + (size_t)gw * ANS * Wk::STAGE;
+      const TT* T = reinterpret_cast<const TT*>(g.T);
+      const int64_t tstride = (int64_t)g.rows * g.d_out;
+      for (int64_t j = gw; j < cnt; j += GW) {
+        const int64_t token = t0 + j;
+        const int slot = (int)(j % R);
+        const uint32_t use = (uint32_t)(j / R);
+        if (!fws::bar_wait(full + slot, use & 1, kLimit)) bad |= kFlagStreamDev;
+        const uint2* rec = reinterpret_cast<const uint2*>(ring + (size_t)slot * rec_slot);
+        float* yr = g.y + token * g.d_out;
+        for (int part = 0; part < fp.parts; ++part) {
+          const int c0 = part * MAXC;
+          bool ok[MAXC];
+#pragma unroll
+          for (int c = 0; c < MAXC; ++c)
+            ok[c] = (c0 + c < nchunks) && (c0 * CHUNK + lane * VEC + c * CHUNK < g.d_out);
+          float acc[MAXC][VEC];
+#pragma unroll
+          for (int c = 0; c < MAXC; ++c)
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) acc[c][v] = 0.f;
+          if (fp.debug_mode != 1)
+            Wk::walk(gring, T + c0 * CHUNK, tstride, g.d_out, hl, lane, ok, acc,
+                     [&](int k) { return rec[k].x; }, [&](int k) { return __uint_as_float(rec[k].y); });
+#pragma unroll
+          for (int c = 0; c < MAXC; ++c) {
+            if (!ok[c]) continue;
+            const int col = (c0 + c) * CHUNK + lane * VEC;
+#pragma unroll
+            for (int v = 0; v < VEC; v += 4) {
+              const float4 o = make_float4(acc[c][v], acc[c][v + 1], acc[c][v + 2], acc[c][v + 3]);
+              if (!isfinite(o.x) || !isfinite(o.y) || !isfinite(o.z) || !isfinite(o.w)) bad |= 4;
+              *reinterpret_cast<float4*>(yr + col + v) = o;
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) fws::bar_arrive(empty + slot);
+      }
+    } else {
     const TT* T = reinterpret_cast<const TT*>(g.T);
     const int64_t tstride = (int64_t)g.rows * g.d_out;
     for (int64_t j = gw; j < cnt; j += GW) {
@@ -273,6 +319,7 @@ __global__ void __launch_bounds__(512, 1) fused_ws_kernel(FusedParams fp) {
           atomicAdd(fp.done + token / fp.chunk_tokens, 1);
         }
       }
+    }
     }
   }
   if (bad) atomicOr(p.flag, bad);

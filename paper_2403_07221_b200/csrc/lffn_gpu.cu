@@ -595,6 +595,29 @@ int launch_gather_group(lffn_ctx* c, const uint32_t* codes, const float* coeff, 
                       (reinterpret_cast<uintptr_t>(p.coeff) % 16 == 0);
     const int64_t warps = n * wpt;
     const unsigned grid = (unsigned)((warps * 32 + 255) / 256);
+    static const char* gasync = getenv("LFFN_GATHER_ASYNC");  // experiment: "TPS,NS,NW"
+    if (gasync && rec4 && !p.accumulate) {
+      int tps = 2, ns = 2, nw = 16;
+      sscanf(gasync, "%d,%d,%d", &tps, &ns, &nw);
+      using AF = void (*)(GatherParams);
+      AF fn = nullptr;
+      int mc = 0;
+#define LFFN_GA(TT, M, TP, NSV, NWV) \
+  if (tps == TP && ns == NSV && nw == NWV) fn = &gather_async_kernel<TT, M, TP, NSV, NWV>, mc = M;
+      if (f32 && nchunks == 6) {
+        LFFN_GA(float, 6, 2, 2, 16) LFFN_GA(float, 6, 1, 3, 16)
+      }
+#undef LFFN_GA
+      if (fn && (p.nk % tps) == 0 && nchunks <= mc) {
+        const size_t smem = size_t(nw) * ns * tps * mc * 32 * 16;
+        set_smem(reinterpret_cast<const void*>(fn), int(smem));
+        const unsigned g = unsigned(std::min<int64_t>(c->num_sms, (n + nw - 1) / nw));
+        fn<<<g, nw * 32, smem, st>>>(p);
+        ++c->launches;
+        LFFN_CUDA(cudaGetLastError());
+        return LFFN_OK;
+      }
+    }
     if (rec4) {
       // persistent row kernel: grid = 2 CTAs per SM; 4 tables' packed rows
       // in flight per lane (the f32 6-chunk case keeps 4 x 6 x 16 B)
@@ -734,6 +757,7 @@ struct FusedChoice {
   FusedFn fn = nullptr;
   int maxc = 0, block = 128;
   int hp = 0, ring = 0;  // warp-specialised kernel: hash pairs, ring slots (0 = same-warp kernel)
+  int gw = 0, ans = 0;   // gather warps; shared-memory row stages per gather warp (0 = registers)
 };
 
 // LFFN_OPT_FUSED 1: warp-specialised fused_ws_kernel (opt-in: measured
@@ -749,6 +773,14 @@ FusedChoice fused_choice(const lffn_ctx* c) {
   if (d_out % (f32 ? 4 : 8) != 0) return f;
   const int64_t nchunks = (d_out + (f32 ? 128 : 256) - 1) / (f32 ? 128 : 256);
   static const int hp = getenv("LFFN_FUSED_HP") ? atoi(getenv("LFFN_FUSED_HP")) : 2;
+  // LFFN_FUSED_ASYNC="GW,NS": gather warps with shared-memory row stages
+  static const char* fa = getenv("LFFN_FUSED_ASYNC");
+  if (fa && f32 && tau == 8 && nchunks == 6) {
+    int gw = 16, ns = 3;
+    sscanf(fa, "%d,%d", &gw, &ns);
+    if (gw == 16 && ns == 3) f = FusedChoice{&fused_ws_kernel<float, 8, 6, 2, 16, 16, 3>, 6, 32 * 20, 2, 16, 16, 3};
+    if (f.fn) return f;
+  }
   constexpr int R = 32;
 #define LFFN_WS(TT, TAU, M)                                                          \
   (hp == 3 ? FusedChoice{&fused_ws_kernel<TT, TAU, M, 3, R>, M, 512, 3, R}           \
@@ -794,6 +826,7 @@ int launch_fused(lffn_ctx* c, const FusedChoice& f, const float* d_x, int64_t n,
     const size_t slot = size_t((c->h_loc * 8 + 15) / 16 * 16);
     smem = size_t(16) * f.ring + size_t(f.hp) * size_t(padded_len(int(c->D))) * sizeof(double) +
            size_t(f.ring) * slot;
+    if (f.ans > 0) smem += size_t(f.gw) * f.ans * f.maxc * 32 * 16;
     grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(int64_t(c->num_sms), (n + 15) / 16)));
   } else {
     return fail(LFFN_ERR_USAGE, "fused forward: no kernel for this shape");
