@@ -1,12 +1,15 @@
 // dense_tcgen05.cuh -- K2: the dense projection z = x W on the 5th-gen
-// tensor cores (tcgen05.mma kind::tf32, accumulator in TMEM), 3xTF32 split
-// for fp32-faithful numerics, fused with the code / coefficient epilogue.
+// tensor cores (accumulator in TMEM) with an fp32-faithful operand split --
+// bf16 x3 (kind::f16, six products; the default when d_in % 8 == 0) or tf32
+// hi / lo (kind::tf32, three products) -- fused with the code / coefficient
+// epilogue.
 //
 // Reference: Projection::forward dense branch (projection.cpp:178-198) and
 // lookup_hash_f32 dense (bench.cpp:122-129), compute_codes / top1_weight
 // (lookup.cpp:81-100, 185-189).
 //
-// Numerics: x = x_hi + x_lo and W = W_hi + W_lo with *_hi = tf32(.) and
+// Numerics (tf32 split; the bf16 x3 split is the same idea with three bf16
+// terms): x = x_hi + x_lo and W = W_hi + W_lo with *_hi = tf32(.) and
 // *_lo = tf32(. - *_hi); D += x_hi W_hi + x_hi W_lo + x_lo W_hi accumulates in
 // fp32 in TMEM.  The error (~1e-6 absolute at c2 scale, below the fp32 path
 // of the reference itself) leaves codes bit-exact wherever |z| exceeds ~1e-5,

@@ -405,7 +405,7 @@ int launch_hash_top1(lffn_ctx* c, const float* d_x, int64_t n, uint32_t* codes, 
     return LFFN_OK;
   }
   if (c->proj.kind == LFFN_PROJ_DENSE && !c->dense_exact && !exact_z && c->dense_ntile > 0) {
-    // tcgen05 3xTF32 GEMM fused with codes / coefficients (dense_tcgen05.cuh)
+    // tcgen05 split-precision GEMM fused with codes / coefficients (dense_tcgen05.cuh)
     DenseParams d{};
     d.x = d_x;
     d.wt64 = c->d_wt64;
@@ -1049,7 +1049,7 @@ int lffn_ctx_create_shard(lffn_ctx** out, int device, int64_t max_tokens, const 
     CK(cudaMalloc(&c->d_W, nw * sizeof(double)));
     CK(cudaMemcpy(c->d_W, blob, nw * sizeof(double), cudaMemcpyHostToDevice));
     CK(cudaMalloc(&c->d_zbuf, size_t(std::max<int64_t>(max_tokens, 1)) * c->code_width * sizeof(double)));
-    // tcgen05 3xTF32 path: N tile = largest multiple of lcm(tau, 16) <= 256
+    // tcgen05 path: N tile = largest multiple of lcm(tau, 16) <= 256
     int64_t l = 16;
     while (l % cfg->code_bits != 0) l += 16;
     const int64_t ncols = c->h_loc * cfg->code_bits;
