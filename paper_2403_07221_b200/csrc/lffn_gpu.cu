@@ -536,6 +536,13 @@ int launch_hash_top1(lffn_ctx* c, const float* d_x, int64_t n, uint32_t* codes, 
     LFFN_CUDA(cudaGetLastError());
     return LFFN_OK;
   }
+  if (nt == 128 && kind == kPreDiag && c->logD == 11 && c->n_transforms == 4) {
+    // acdc depth 2 at D = 2048: the same compile-time geometry
+    go(hash_structured_kernel<6, kPreDiag, 128, 3, 11, 4>);
+    ++c->launches;
+    LFFN_CUDA(cudaGetLastError());
+    return LFFN_OK;
+  }
 #define LFFN_HASH_CASE(L)                                              \
   case L:                                                              \
     if (kind == kPreSign) go(hash_structured_kernel<L, kPreSign>);     \
