@@ -754,12 +754,39 @@ __global__ void rows_blockdiag_kernel(const double* __restrict__ in, double* __r
 
 // out[j] = sum_i A[i][j] * G[i][j], i ascending from 0.0 (the reference's
 // per-row accumulation of ga / gd, projection.cpp:345-356)
-__global__ void colsum_prod_kernel(const double* __restrict__ A, const double* __restrict__ G,
-                                   int64_t n, int D, double* __restrict__ out) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(32) colsum_prod_kernel(const double* __restrict__ A,
+                                                         const double* __restrict__ G, int64_t n, int D,
+                                                         double* __restrict__ out) {
+  // out[j] = sum_i A[i][j] * G[i][j], i ascending from 0.0 with separate
+  // multiply and add (the reference's order).  Only the D columns are
+  // independent, so each thread keeps the next U rows' operands in flight
+  // (double-buffered registers) while it folds the current U in order.
+  constexpr int U = 16;
+  const int j = blockIdx.x * 32 + threadIdx.x;
   if (j >= D) return;
+  double a[U], g[U], an[U], gn[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    a[u] = u < n ? A[(int64_t)u * D + j] : 0.0;
+    g[u] = u < n ? G[(int64_t)u * D + j] : 0.0;
+  }
   double acc = 0.0;
-  for (int64_t i = 0; i < n; ++i) acc = __dadd_rn(acc, __dmul_rn(A[i * D + j], G[i * D + j]));
+  for (int64_t i0 = 0; i0 < n; i0 += U) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + U + u;
+      an[u] = i < n ? A[i * D + j] : 0.0;
+      gn[u] = i < n ? G[i * D + j] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (i0 + u < n) acc = __dadd_rn(acc, __dmul_rn(a[u], g[u]));
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      a[u] = an[u];
+      g[u] = gn[u];
+    }
+  }
   out[j] = acc;
 }
 

@@ -1379,14 +1379,14 @@ int launch_proj_backward_stagewise(lffn_ctx* c, const float* d_x, const double* 
       const double* a = c->d_diag + 2 * s * D;
       if (int rc = launch_rows_fwht(c, G, n, st)) return rc;
       if (d_grad_proj) {
-        colsum_prod_kernel<<<unsigned((D + 127) / 128), 128, 0, st>>>(S + size_t(2 * s + 1) * rows, G, n, int(D),
+        colsum_prod_kernel<<<unsigned((D + 31) / 32), 32, 0, st>>>(S + size_t(2 * s + 1) * rows, G, n, int(D),
                                                                         d_grad_proj + (2 * s + 1) * D);
         ++c->launches;
       }
       rows_scale_kernel<<<ge, 256, 0, st>>>(G, n, int(D), a + D);
       if (int rc = launch_rows_fwht(c, G, n, st)) return rc;
       if (d_grad_proj) {
-        colsum_prod_kernel<<<unsigned((D + 127) / 128), 128, 0, st>>>(S + size_t(2 * s) * rows, G, n, int(D),
+        colsum_prod_kernel<<<unsigned((D + 31) / 32), 32, 0, st>>>(S + size_t(2 * s) * rows, G, n, int(D),
                                                                         d_grad_proj + 2 * s * D);
         ++c->launches;
       }
