@@ -752,6 +752,115 @@ __global__ void rows_blockdiag_kernel(const double* __restrict__ in, double* __r
   }
 }
 
+// The same exact GEMM with 32 x 32 tiles (4 x 4 outputs per thread, 64
+// threads): four times the tiles of gemm_f64_exact8_kernel for GEMMs with few
+// output tiles and a long sequential K (the bh parameter gradient: 32 blocks
+// of 64 x 64 summed over all tokens).  Bit-identical sums.
+template <typename TA, bool TRANS_A, bool TRANS_B>
+__global__ void __launch_bounds__(64) gemm_f64_exact4_kernel(const TA* __restrict__ A, int lda,
+                                                             const double* __restrict__ B, int ldb,
+                                                             double* __restrict__ C, int ldc, int M,
+                                                             int N, int K, int* flag, int64_t sA = 0,
+                                                             int64_t sB = 0, int64_t sC = 0) {
+  A += blockIdx.z * sA;
+  B += blockIdx.z * sB;
+  C += blockIdx.z * sC;
+  int bad = 0;
+  __shared__ double As[2][8][33];
+  __shared__ double Bs[2][8][33];
+  const int t = threadIdx.x;
+  const int tx = t & 7, ty = t >> 3;
+  const int m0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
+  auto load_a = [&](int k0, double (&r)[4]) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int kk = TRANS_A ? (t >> 5) + 2 * i : (t & 7);
+      const int mm = TRANS_A ? (t & 31) : (t >> 3) + 8 * i;
+      const int gm = m0 + mm, gk = k0 + kk;
+      r[i] = (gm < M && gk < K) ? (double)(TRANS_A ? A[(int64_t)gk * lda + gm] : A[(int64_t)gm * lda + gk])
+                                : 0.0;
+    }
+  };
+  auto load_b = [&](int k0, double (&r)[4]) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int kk = TRANS_B ? (t & 7) : (t >> 5) + 2 * i;
+      const int nn = TRANS_B ? (t >> 3) + 8 * i : (t & 31);
+      const int gn = n0 + nn, gk = k0 + kk;
+      r[i] = (gn < N && gk < K) ? (TRANS_B ? B[(int64_t)gn * ldb + gk] : B[(int64_t)gk * ldb + gn]) : 0.0;
+    }
+  };
+  auto store = [&](int buf, const double (&ra)[4], const double (&rb)[4]) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      As[buf][TRANS_A ? (t >> 5) + 2 * i : (t & 7)][TRANS_A ? (t & 31) : (t >> 3) + 8 * i] = ra[i];
+      Bs[buf][TRANS_B ? (t & 7) : (t >> 5) + 2 * i][TRANS_B ? (t >> 3) + 8 * i : (t & 31)] = rb[i];
+    }
+  };
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  double ra[4], rb[4];
+  load_a(0, ra);
+  load_b(0, rb);
+  store(0, ra, rb);
+  __syncthreads();
+  int buf = 0;
+  for (int k0 = 0; k0 < K; k0 += 8) {
+    const bool more = k0 + 8 < K;
+    if (more) {
+      load_a(k0 + 8, ra);
+      load_b(k0 + 8, rb);
+    }
+    const int kmax = min(8, K - k0);
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      if (kk < kmax) {
+        double a[4], b[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = As[buf][kk][ty + 8 * i];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[j] = Bs[buf][kk][tx + 8 * j];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = __dadd_rn(acc[i][j], __dmul_rn(a[i], b[j]));
+      }
+    }
+    if (more) {
+      store(buf ^ 1, ra, rb);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gm = m0 + ty + 8 * i, gn = n0 + tx + 8 * j;
+      if (gm < M && gn < N) {
+        if (!isfinite(acc[i][j])) bad |= kFlagBwdOutput;
+        C[(int64_t)gm * ldc + gn] = acc[i][j];
+      }
+    }
+  if (bad && flag) atomicOr(flag, bad);
+}
+
+// BT[k] = B[k]^T for nblk square b x b blocks (the bh backward multiplies by
+// B_g^T through the coalesced non-transposed row kernel)
+__global__ void blocks_transpose_kernel(const double* __restrict__ B, double* __restrict__ BT,
+                                        int64_t nblk, int b) {
+  const int64_t bb = (int64_t)b * b;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nblk * bb;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = q / bb;
+    const int r = int((q - k * bb) / b), cc = int(q - k * bb - (int64_t)r * b);
+    BT[k * bb + (int64_t)cc * b + r] = B[q];
+  }
+}
+
 // out[j] = sum_i A[i][j] * G[i][j], i ascending from 0.0 (the reference's
 // per-row accumulation of ga / gd, projection.cpp:345-356)
 __global__ void __launch_bounds__(32) colsum_prod_kernel(const double* __restrict__ A,

@@ -80,6 +80,7 @@ struct lffn_ctx {
   double* d_diag = nullptr;
   double* d_W = nullptr;
   double* d_bh = nullptr;   // bh: m x (D/b) x b x b blocks (float64)
+  double* d_bhT = nullptr;  // bh backward: the same blocks, each transposed (built on first use)
   void* d_wp[3] = {nullptr, nullptr, nullptr};  // dense (tcgen05): W^T slice split planes
   double* d_wt64 = nullptr;  // dense: slice of W^T in float64 (exact near-zero fixups)
   int dense_ntile = 0;       // N tile of the tcgen05 dense GEMM (0: exact path only)
@@ -171,6 +172,7 @@ void destroy_ctx(lffn_ctx* c) {
   cudaFree(c->d_diag);
   cudaFree(c->d_W);
   cudaFree(c->d_bh);
+  cudaFree(c->d_bhT);
   for (int q = 0; q < 3; ++q) cudaFree(c->d_wp[q]);
   cudaFree(c->d_wt64);
   for (int q = 0; q < 3; ++q) cudaFree(c->d_xp[q]);
@@ -1350,6 +1352,13 @@ int launch_proj_backward_stagewise(lffn_ctx* c, const float* d_x, const double* 
   const unsigned ge = unsigned(std::min<int64_t>(int64_t(c->num_sms) * 16, (n * D + 255) / 256));
   const int b = int(c->proj.block == 0 ? D : c->proj.block);
   const int64_t stage_size = (D / b) * b * b;
+  if (!acdc && !c->d_bhT) {
+    const int64_t total = int64_t(nst) * stage_size;
+    LFFN_CUDA(cudaMalloc(&c->d_bhT, size_t(total) * sizeof(double)));
+    blocks_transpose_kernel<<<unsigned(std::min<int64_t>(int64_t(c->num_sms) * 8, (total + 255) / 256)), 256, 0,
+                              st>>>(c->d_bh, c->d_bhT, total / (int64_t(b) * b), b);
+    ++c->launches;
+  }
   // forward: the stage inputs (projection.cpp:216-245)
   rows_pad_kernel<<<ge, 256, 0, st>>>(d_x, n, int(c->cfg.d_in), int(D), V);
   ++c->launches;
@@ -1396,13 +1405,15 @@ int launch_proj_backward_stagewise(lffn_ctx* c, const float* d_x, const double* 
       if (int rc = launch_rows_fwht(c, G, n, st)) return rc;
       if (d_grad_proj) {
         // grad_B_s[g][r][c] = sum_i src_i[g*b + r] * g_i[g*b + c], tokens ascending
-        dim3 grid(unsigned((b + 63) / 64), unsigned((b + 63) / 64), unsigned(D / b));
-        gemm_f64_exact8_kernel<double, true, false><<<grid, 64, 0, st>>>(
+        dim3 grid(unsigned((b + 31) / 32), unsigned((b + 31) / 32), unsigned(D / b));
+        gemm_f64_exact4_kernel<double, true, false><<<grid, 64, 0, st>>>(
             S + size_t(s) * rows, int(D), G, int(D), d_grad_proj + s * stage_size, b, b, b, int(n),
             c->d_flag, b, b, int64_t(b) * b);
         ++c->launches;
       }
-      rows_blockdiag_kernel<true><<<ge, 256, 0, st>>>(G, V, n, int(D), b, c->d_bh + s * stage_size);
+      // x B_g^T through the transposed copy: the coalesced (non-transposed)
+      // row kernel, same products and the same summation order
+      rows_blockdiag_kernel<false><<<ge, 256, 0, st>>>(G, V, n, int(D), b, c->d_bhT + s * stage_size);
       std::swap(V, G);
       ++c->launches;
     }
