@@ -1438,9 +1438,20 @@ int launch_proj_backward(lffn_ctx* c, const float* d_x, const double* gz, int64_
       ++c->launches;
     }
     if (d_grad_proj) {
-      dim3 grid(unsigned((cw + 63) / 64), unsigned((d_in + 63) / 64));
-      gemm_f64_exact8_kernel<float, true, false><<<grid, 64, 0, st>>>(d_x, d_in, gz, cw, d_grad_proj, cw,
-                                                                     d_in, cw, int(n), c->d_flag);
+      // grad_W = x^T g: its K (tokens) must stay sequential, so the output
+      // tiles are all the parallelism -- 32 x 32 tiles when 64 x 64 ones
+      // would not fill the SMs a few times over
+      static const int gw4 = getenv("LFFN_GRADW_TILE32") ? atoi(getenv("LFFN_GRADW_TILE32")) : 1;
+      const int64_t tiles64 = int64_t((cw + 63) / 64) * ((d_in + 63) / 64);
+      if (gw4 && tiles64 < int64_t(c->num_sms) * 8) {
+        dim3 grid(unsigned((cw + 31) / 32), unsigned((d_in + 31) / 32));
+        gemm_f64_exact4_kernel<float, true, false><<<grid, 64, 0, st>>>(d_x, d_in, gz, cw, d_grad_proj, cw,
+                                                                       d_in, cw, int(n), c->d_flag);
+      } else {
+        dim3 grid(unsigned((cw + 63) / 64), unsigned((d_in + 63) / 64));
+        gemm_f64_exact8_kernel<float, true, false><<<grid, 64, 0, st>>>(d_x, d_in, gz, cw, d_grad_proj, cw,
+                                                                       d_in, cw, int(n), c->d_flag);
+      }
       ++c->launches;
     }
     LFFN_CUDA(cudaGetLastError());
