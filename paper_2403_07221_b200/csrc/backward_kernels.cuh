@@ -900,15 +900,16 @@ __global__ void __launch_bounds__(32) colsum_prod_kernel(const double* __restric
 }
 
 // in-place FWHT of every row (fwht.hpp:28-41), K1's phases in shared memory
-template <int LOGE>
-__global__ void __launch_bounds__(256) rows_fwht_kernel(HashParams p, double* __restrict__ V) {
+template <int LOGE, int NT = 256, int MINB = 1, int LOGD = 0>
+__global__ void __launch_bounds__(NT, MINB) rows_fwht_kernel(HashParams p, double* __restrict__ V) {
   extern __shared__ double smem[];
-  const int tpt = p.threads_per_token;
+  const int tpt = LOGD > 0 ? (1 << (LOGD - LOGE)) : p.threads_per_token;
   const int slot = threadIdx.x / tpt;
   const int t = threadIdx.x - slot * tpt;
   const int64_t token = (int64_t)blockIdx.x * p.tokens_per_block + slot;
   const bool active = slot < p.tokens_per_block && token < p.n;
-  const int D = p.D;
+  const int logD = LOGD > 0 ? LOGD : p.logD;
+  const int D = 1 << logD;
   double* sm = smem + (size_t)slot * padded_len(D);
   int bad = 0;
   auto token_sync = [&]() {
@@ -919,11 +920,13 @@ __global__ void __launch_bounds__(256) rows_fwht_kernel(HashParams p, double* __
     for (int a = t; a < D; a += tpt) sm[spos(a)] = V[token * D + a];
   token_sync();
   int nph = 1;
-  if constexpr (LOGE > 0) nph = (p.logD + LOGE - 1) / LOGE;
+  if constexpr (LOGE > 0) nph = (logD + LOGE - 1) / LOGE;
   if (active) phase_smem<LOGE, LOGE, false, kPreNone>(sm, t, tpt, 0, p, 0, nullptr, bad, false);
   token_sync();
-  for (int ph = 1; ph < nph; ++ph) {
-    if (active) run_later_phase<LOGE>(sm, t, tpt, ph * LOGE, min(LOGE, p.logD - ph * LOGE), p, 0, bad, false);
+  const int nphc = LOGD > 0 ? (LOGD + LOGE - 1) / LOGE : nph;
+#pragma unroll
+  for (int ph = 1; ph < nphc; ++ph) {
+    if (active) run_later_phase<LOGE>(sm, t, tpt, ph * LOGE, min(LOGE, logD - ph * LOGE), p, 0, bad, false);
     token_sync();
   }
   if (active)

@@ -1311,7 +1311,9 @@ int launch_rows_fwht(lffn_ctx* c, double* V, int64_t n, cudaStream_t st) {
   p.flag = c->d_flag;
   const int loge = c->logD >= kMaxLogE ? kMaxLogE : int(c->logD);
   const int tpt = int(c->D >> loge);
-  const int block = std::max(tpt, (256 / tpt) * tpt);
+  // D = 2048: compile-time geometry, 128-thread CTAs, 3 per SM (as K1)
+  const bool fixed = loge == 6 && c->logD == 11;
+  const int block = std::max(tpt, ((fixed ? 128 : 256) / tpt) * tpt);
   const int tpb = block / tpt;
   p.tokens_per_block = tpb;
   p.threads_per_token = tpt;
@@ -1321,6 +1323,12 @@ int launch_rows_fwht(lffn_ctx* c, double* V, int64_t n, cudaStream_t st) {
     set_smem(reinterpret_cast<const void*>(kernel), int(smem));
     kernel<<<grid, block, smem, st>>>(p, V);
   };
+  if (fixed) {
+    go(rows_fwht_kernel<6, 128, 3, 11>);
+    ++c->launches;
+    LFFN_CUDA(cudaGetLastError());
+    return LFFN_OK;
+  }
   switch (loge) {
     case 0: go(rows_fwht_kernel<0>); break;
     case 1: go(rows_fwht_kernel<1>); break;
