@@ -265,11 +265,22 @@ __global__ void __launch_bounds__(256) bwd_gz_kernel(BwdParams p, const double* 
   const int tau = TAU > 0 ? TAU : p.tau;
   const double* zk = p.z + token * p.code_width + (int64_t)(p.kb + k) * tau;
   double zv[TAU > 0 ? TAU : 24];
+  if constexpr (TAU > 0 && TAU % 2 == 0) {
+    // 16-byte loads (the table's tau coordinates are contiguous and 16-byte
+    // aligned for even tau)
+#pragma unroll
+    for (int j = 0; j < TAU; j += 2) {
+      const double2 q = *reinterpret_cast<const double2*>(zk + j);
+      zv[j] = q.x;
+      zv[j + 1] = q.y;
+    }
+  } else {
+    for (int j = 0; j < tau; ++j) zv[j] = zk[j];
+  }
   double sum_abs = 0.0, w1 = 1.0, logden = 0.0;
 #pragma unroll
   for (int j = 0; j < tau; ++j) {
-    const double zj = zk[j];
-    zv[j] = zj;
+    const double zj = zv[j];
     const double aj = fabs(zj);
     sum_abs = sum_abs + aj;
     // 1 + exp(-2a) == 1.0 exactly for a >= 18.5: the division is then exact
@@ -300,8 +311,12 @@ __global__ void __launch_bounds__(256) bwd_gz_kernel(BwdParams p, const double* 
     }
   }
   double* gz = p.gz + token * p.code_width + (int64_t)(p.kb + k) * tau;
+  if constexpr (TAU > 0 && TAU % 2 == 0) {
 #pragma unroll
-  for (int j = 0; j < tau; ++j) gz[j] = gzv[j];
+    for (int j = 0; j < TAU; j += 2) *reinterpret_cast<double2*>(gz + j) = make_double2(gzv[j], gzv[j + 1]);
+  } else {
+    for (int j = 0; j < tau; ++j) gz[j] = gzv[j];
+  }
 }
 
 // KB2a: deterministic ranks.  Thread (k, b) walks token block b in order
