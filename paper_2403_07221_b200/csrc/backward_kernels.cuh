@@ -436,18 +436,24 @@ __global__ void bwd_place_kernel(BwdParams p, const uint32_t* hist, const uint32
 // a time so four grad_y rows are in flight; per column the products are
 // accumulated in record order exactly as bwd_gradT_kernel -- bit-identical.
 template <int MAXC>
-__global__ void __launch_bounds__(256) bwd_gradT4_kernel(BwdParams p) {
+__global__ void __launch_bounds__(256) bwd_gradT4_kernel(BwdParams p, int parts) {
+  // a row's columns are split into `parts` warps of MAXC chunks each (wide
+  // rows would otherwise need > 128 registers); per column the order is the
+  // same
   const int lane = threadIdx.x & 31;
-  const int64_t bin = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t bin = gw / parts;
+  const int part = (int)(gw - bin * parts);
   const int64_t bins = (int64_t)p.hl * p.rows;
   if (bin >= bins) return;
   const uint32_t b0 = p.offs[bin], b1 = p.offs[bin + 1];
   const int per_tok = p.hl * p.nc;
+  const int cbase = part * MAXC * 128;  // first column of this warp's part
   bool ok[MAXC];
   float4 acc[MAXC];
 #pragma unroll
   for (int c = 0; c < MAXC; ++c) {
-    ok[c] = c * 128 + lane * 4 < p.d_out;
+    ok[c] = cbase + c * 128 + lane * 4 < p.d_out;
     acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   for (uint32_t e0 = b0; e0 < b1; e0 += 4) {
@@ -458,7 +464,7 @@ __global__ void __launch_bounds__(256) bwd_gradT4_kernel(BwdParams p) {
       const uint32_t e = min(e0 + q, b1 - 1);
       const uint32_t rec = __ldg(p.list + e);
       cf[q] = e0 + q < b1 ? __ldg(p.coeff + rec) : 0.f;
-      gyr[q] = p.gy + (int64_t)(rec / per_tok) * p.d_out + lane * 4;
+      gyr[q] = p.gy + (int64_t)(rec / per_tok) * p.d_out + cbase + lane * 4;
     }
     float4 g[4][MAXC];
 #pragma unroll
@@ -480,7 +486,7 @@ __global__ void __launch_bounds__(256) bwd_gradT4_kernel(BwdParams p) {
     }
   }
   int bad = 0;
-  float* out = p.gT + bin * p.d_out + lane * 4;
+  float* out = p.gT + bin * p.d_out + cbase + lane * 4;
 #pragma unroll
   for (int c = 0; c < MAXC; ++c) {
     if (!ok[c]) continue;

@@ -1581,7 +1581,7 @@ int lffn_backward(lffn_ctx* c, const float* d_x, const float* d_grad_y, int64_t 
       if (v4 && mc <= 8 && c->cfg.code_bits <= 24 && !one_pass) {
         // KB1a gdot per record (many rows in flight), KB1b gz per (token, table)
         const unsigned gg = unsigned(std::min<int64_t>(int64_t(c->num_sms) * 2, (n * 32 + 255) / 256));
-#define LFFN_GDOT(TT, M) bwd_gdot_kernel<TT, M, (M >= 6 ? 2 : 4)><<<gg, 256, 0, st>>>(p, c->d_bwd_gdot)
+#define LFFN_GDOT(TT, M) bwd_gdot_kernel<TT, M, (M >= 8 ? 1 : M >= 6 ? 2 : 4)><<<gg, 256, 0, st>>>(p, c->d_bwd_gdot)
         if (esz == 4) {
           if (mc <= 2) LFFN_GDOT(float, 2); else if (mc <= 4) LFFN_GDOT(float, 4);
           else if (mc <= 6) LFFN_GDOT(float, 6); else LFFN_GDOT(float, 8);
@@ -1615,11 +1615,14 @@ int lffn_backward(lffn_ctx* c, const float* d_x, const float* d_grad_y, int64_t 
       bwd_place_kernel<<<gr, 256, 0, st>>>(p, c->d_bwd_hist, c->d_bwd_rank);
       const unsigned gt = unsigned((bins * 32 + 255) / 256);
       const int mc4 = int((c->cfg.d_out + 127) / 128);
-      if (c->cfg.d_out % 4 == 0 && mc4 <= 8) {
-        if (mc4 <= 2) bwd_gradT4_kernel<2><<<gt, 256, 0, st>>>(p);
-        else if (mc4 <= 4) bwd_gradT4_kernel<4><<<gt, 256, 0, st>>>(p);
-        else if (mc4 <= 6) bwd_gradT4_kernel<6><<<gt, 256, 0, st>>>(p);
-        else bwd_gradT4_kernel<8><<<gt, 256, 0, st>>>(p);
+      if (c->cfg.d_out % 4 == 0) {
+        if (mc4 <= 2) bwd_gradT4_kernel<2><<<gt, 256, 0, st>>>(p, 1);
+        else if (mc4 <= 4) bwd_gradT4_kernel<4><<<gt, 256, 0, st>>>(p, 1);
+        else if (mc4 <= 6) bwd_gradT4_kernel<6><<<gt, 256, 0, st>>>(p, 1);
+        else {
+          const int parts = (mc4 + 3) / 4;
+          bwd_gradT4_kernel<4><<<unsigned((bins * parts * 32 + 255) / 256), 256, 0, st>>>(p, parts);
+        }
       } else {
         bwd_gradT_kernel<<<gt, 256, 0, st>>>(p);
       }
