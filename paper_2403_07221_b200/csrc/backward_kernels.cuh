@@ -106,7 +106,22 @@ __global__ void __launch_bounds__(256) bwd_gradz_kernel(BwdParams p) {
       const uint32_t code = p.codes[rec];
       const TT* row = T + ((int64_t)k * p.rows + code) * p.d_out;
       float part = 0.f;
-      if constexpr (VEC == 4) {
+      if constexpr (VEC == 8) {
+        // bf16 rows, 16-byte loads: lane l owns columns 256 i + 8 l .. + 7
+        for (int j = lane * 8; j < p.d_out; j += 256) {
+          const float4 ga = *reinterpret_cast<const float4*>(gyr + j);
+          const float4 gb = *reinterpret_cast<const float4*>(gyr + j + 4);
+          const uint4 u = __ldg(reinterpret_cast<const uint4*>(row + j));
+          part = fmaf(ga.x, __uint_as_float(u.x << 16), part);
+          part = fmaf(ga.y, __uint_as_float(u.x & 0xffff0000u), part);
+          part = fmaf(ga.z, __uint_as_float(u.y << 16), part);
+          part = fmaf(ga.w, __uint_as_float(u.y & 0xffff0000u), part);
+          part = fmaf(gb.x, __uint_as_float(u.z << 16), part);
+          part = fmaf(gb.y, __uint_as_float(u.z & 0xffff0000u), part);
+          part = fmaf(gb.z, __uint_as_float(u.w << 16), part);
+          part = fmaf(gb.w, __uint_as_float(u.w & 0xffff0000u), part);
+        }
+      } else if constexpr (VEC == 4) {
         for (int j = lane * 4; j < p.d_out; j += 128) {
           const float4 g = *reinterpret_cast<const float4*>(gyr + j);
           float t0, t1, t2, t3;
@@ -162,9 +177,14 @@ __global__ void __launch_bounds__(256) bwd_gradz_kernel(BwdParams p) {
 // partials are reduced across the warp in float64 with a transposed
 // butterfly (31 exchanges for 32 sums instead of 5 per record), after which
 // lane l holds record l's sum and the 32 results are stored coalesced.
-template <typename TT, int MAXC, int TIF>
+template <typename TT, int MAXC, int TIF, int VEC = 4>
 __global__ void __launch_bounds__(256, 2) bwd_gdot_kernel(BwdParams p, double* gdot) {
+  // VEC columns per lane per chunk: 4 (fp32 rows, 16-byte loads; bf16 rows,
+  // 8-byte loads) or 8 (bf16 rows, 16-byte loads) -- the same per-lane
+  // column order as bwd_gradz_kernel<TT, VEC>
   static_assert(32 % TIF == 0, "TIF must divide 32");
+  static_assert(VEC == 4 || (VEC == 8 && sizeof(TT) == 2), "VEC 8 is for bf16 rows");
+  constexpr int CW = 32 * VEC;  // columns per chunk
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const TT* T = static_cast<const TT*>(p.T);
@@ -173,15 +193,18 @@ __global__ void __launch_bounds__(256, 2) bwd_gdot_kernel(BwdParams p, double* g
   for (int64_t token = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; token < p.n;
        token += nwarps) {
     const float* gyr = p.gy + token * p.d_out;
-    float4 g[MAXC];
+    float g[MAXC][VEC];
     bool ok[MAXC];
 #pragma unroll
     for (int c = 0; c < MAXC; ++c) {
-      const int j = c * 128 + lane * 4;
+      const int j = c * CW + lane * VEC;
       ok[c] = j < p.d_out;
-      g[c] = ok[c] ? *reinterpret_cast<const float4*>(gyr + j) : make_float4(0.f, 0.f, 0.f, 0.f);
-      if (!isfinite(g[c].x) || !isfinite(g[c].y) || !isfinite(g[c].z) || !isfinite(g[c].w))
-        bad |= kFlagBwdInput;
+#pragma unroll
+      for (int v = 0; v < VEC; v += 4) {
+        const float4 q = ok[c] ? *reinterpret_cast<const float4*>(gyr + j + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+        g[c][v] = q.x; g[c][v + 1] = q.y; g[c][v + 2] = q.z; g[c][v + 3] = q.w;
+        if (!isfinite(q.x) || !isfinite(q.y) || !isfinite(q.z) || !isfinite(q.w)) bad |= kFlagBwdInput;
+      }
     }
     const uint32_t* cr = p.codes + token * R;
     for (int r32 = 0; r32 < R; r32 += 32) {
@@ -190,25 +213,27 @@ __global__ void __launch_bounds__(256, 2) bwd_gdot_kernel(BwdParams p, double* g
       float part[32];
 #pragma unroll
       for (int q0 = 0; q0 < 32; q0 += TIF) {
-        float4 t4[TIF][MAXC];
+        // raw rows in flight (bf16 VEC 8: packed, widened at the FMA)
+        float t[sizeof(TT) == 2 && VEC == 8 ? 1 : TIF][MAXC][VEC];
+        uint4 traw[sizeof(TT) == 2 && VEC == 8 ? TIF : 1][MAXC];
 #pragma unroll
         for (int q = 0; q < TIF; ++q) {
           const int r = r32 + q0 + q;
           const uint32_t code = __shfl_sync(0xffffffffu, mycode, q0 + q);
           const int k = p.nc == 1 ? r : r / p.nc;
-          const TT* row = T + ((int64_t)k * p.rows + code) * p.d_out + lane * 4;
+          const TT* row = T + ((int64_t)k * p.rows + code) * p.d_out + lane * VEC;
 #pragma unroll
           for (int c = 0; c < MAXC; ++c) {
-            if (ok[c] && r < R) {
-              if constexpr (sizeof(TT) == 4) {
-                t4[q][c] = __ldg(reinterpret_cast<const float4*>(row + c * 128));
-              } else {
-                const uint2 u = __ldg(reinterpret_cast<const uint2*>(row + c * 128));
-                t4[q][c] = make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xffff0000u),
-                                       __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xffff0000u));
-              }
+            const bool on = ok[c] && r < R;
+            if constexpr (sizeof(TT) == 4) {
+              const float4 u = on ? __ldg(reinterpret_cast<const float4*>(row + c * CW)) : make_float4(0.f, 0.f, 0.f, 0.f);
+              t[q][c][0] = u.x; t[q][c][1] = u.y; t[q][c][2] = u.z; t[q][c][3] = u.w;
+            } else if constexpr (VEC == 4) {
+              const uint2 u = on ? __ldg(reinterpret_cast<const uint2*>(row + c * CW)) : make_uint2(0u, 0u);
+              t[q][c][0] = __uint_as_float(u.x << 16); t[q][c][1] = __uint_as_float(u.x & 0xffff0000u);
+              t[q][c][2] = __uint_as_float(u.y << 16); t[q][c][3] = __uint_as_float(u.y & 0xffff0000u);
             } else {
-              t4[q][c] = make_float4(0.f, 0.f, 0.f, 0.f);
+              traw[q][c] = on ? __ldg(reinterpret_cast<const uint4*>(row + c * CW)) : make_uint4(0u, 0u, 0u, 0u);
             }
           }
         }
@@ -217,10 +242,17 @@ __global__ void __launch_bounds__(256, 2) bwd_gdot_kernel(BwdParams p, double* g
           float acc = 0.f;
 #pragma unroll
           for (int c = 0; c < MAXC; ++c) {
-            acc = fmaf(g[c].x, t4[q][c].x, acc);
-            acc = fmaf(g[c].y, t4[q][c].y, acc);
-            acc = fmaf(g[c].z, t4[q][c].z, acc);
-            acc = fmaf(g[c].w, t4[q][c].w, acc);
+            if constexpr (sizeof(TT) == 2 && VEC == 8) {
+              const uint32_t w4[4] = {traw[q][c].x, traw[q][c].y, traw[q][c].z, traw[q][c].w};
+#pragma unroll
+              for (int h = 0; h < 4; ++h) {
+                acc = fmaf(g[c][2 * h], __uint_as_float(w4[h] << 16), acc);
+                acc = fmaf(g[c][2 * h + 1], __uint_as_float(w4[h] & 0xffff0000u), acc);
+              }
+            } else {
+#pragma unroll
+              for (int v = 0; v < VEC; ++v) acc = fmaf(g[c][v], t[q][c][v], acc);
+            }
           }
           part[q0 + q] = acc;
         }

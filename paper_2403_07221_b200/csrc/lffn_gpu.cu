@@ -1576,18 +1576,26 @@ int lffn_backward(lffn_ctx* c, const float* d_x, const float* d_grad_y, int64_t 
     if (c->h_loc > 0) {
       const unsigned g1 = unsigned((n * 32 + 255) / 256);
       const bool v4 = c->cfg.d_out % 4 == 0;
-      const int mc = int((c->cfg.d_out + 127) / 128);  // 4-column chunks per lane
+      // bf16 rows with d_out % 8 == 0: 8 columns per lane per chunk (16-byte
+      // loads); otherwise 4 (fp32 16-byte / bf16 8-byte loads)
+      const bool v8 = esz == 2 && c->cfg.d_out % 8 == 0;
+      const int mc = int((c->cfg.d_out + (v8 ? 255 : 127)) / (v8 ? 256 : 128));  // chunks per lane
       static const int one_pass = getenv("LFFN_BWD_ONE_PASS") ? atoi(getenv("LFFN_BWD_ONE_PASS")) : 0;
-      if (v4 && mc <= 8 && c->cfg.code_bits <= 24 && !one_pass) {
+      if (v4 && mc <= (v8 ? 4 : 8) && c->cfg.code_bits <= 24 && !one_pass) {
         // KB1a gdot per record (many rows in flight), KB1b gz per (token, table)
         const unsigned gg = unsigned(std::min<int64_t>(int64_t(c->num_sms) * 2, (n * 32 + 255) / 256));
-#define LFFN_GDOT(TT, M) bwd_gdot_kernel<TT, M, (M >= 8 ? 1 : M >= 6 ? 2 : 4)><<<gg, 256, 0, st>>>(p, c->d_bwd_gdot)
+#define LFFN_GDOT(TT, M, V) \
+  bwd_gdot_kernel<TT, M, ((M) * (V) >= 32 ? 1 : (M) * (V) >= 24 ? 2 : 4), V><<<gg, 256, 0, st>>>(p, c->d_bwd_gdot)
         if (esz == 4) {
-          if (mc <= 2) LFFN_GDOT(float, 2); else if (mc <= 4) LFFN_GDOT(float, 4);
-          else if (mc <= 6) LFFN_GDOT(float, 6); else LFFN_GDOT(float, 8);
+          if (mc <= 2) LFFN_GDOT(float, 2, 4); else if (mc <= 4) LFFN_GDOT(float, 4, 4);
+          else if (mc <= 6) LFFN_GDOT(float, 6, 4); else LFFN_GDOT(float, 8, 4);
+        } else if (v8) {
+          // packed rows in flight: TIF 4 / 2 at 2 / 4 chunks
+          if (mc <= 2) bwd_gdot_kernel<__nv_bfloat16, 2, 4, 8><<<gg, 256, 0, st>>>(p, c->d_bwd_gdot);
+          else bwd_gdot_kernel<__nv_bfloat16, 4, 2, 8><<<gg, 256, 0, st>>>(p, c->d_bwd_gdot);
         } else {
-          if (mc <= 2) LFFN_GDOT(__nv_bfloat16, 2); else if (mc <= 4) LFFN_GDOT(__nv_bfloat16, 4);
-          else if (mc <= 6) LFFN_GDOT(__nv_bfloat16, 6); else LFFN_GDOT(__nv_bfloat16, 8);
+          if (mc <= 2) LFFN_GDOT(__nv_bfloat16, 2, 4); else if (mc <= 4) LFFN_GDOT(__nv_bfloat16, 4, 4);
+          else if (mc <= 6) LFFN_GDOT(__nv_bfloat16, 6, 4); else LFFN_GDOT(__nv_bfloat16, 8, 4);
         }
 #undef LFFN_GDOT
         const unsigned gz = unsigned((n * c->h_loc + 255) / 256);
@@ -1598,6 +1606,7 @@ int lffn_backward(lffn_ctx* c, const float* d_x, const float* d_grad_y, int64_t 
       } else {
         if (esz == 4 && v4) bwd_gradz_kernel<float, 4><<<g1, 256, 0, st>>>(p);
         else if (esz == 4) bwd_gradz_kernel<float, 1><<<g1, 256, 0, st>>>(p);
+        else if (v8) bwd_gradz_kernel<__nv_bfloat16, 8><<<g1, 256, 0, st>>>(p);
         else if (v4) bwd_gradz_kernel<__nv_bfloat16, 4><<<g1, 256, 0, st>>>(p);
         else bwd_gradz_kernel<__nv_bfloat16, 1><<<g1, 256, 0, st>>>(p);
         ++c->launches;
