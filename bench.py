@@ -467,7 +467,10 @@ def run_ours(args):
                 "peak": round(peak_eff, 1),
                 "unit": "GB/s",
                 "frac": round(achieved / peak_eff, 4),
-                "traffic": traffic,
+                # dram__bytes_read.sum + dram__bytes_write.sum of the gather
+                # launch, bytes, from the committed ncu --set full capture
+                "traffic": (traffic or {}).get("dram_bytes_per_launch"),
+                "traffic_source": (traffic or {}).get("source"),
                 "definition": "BASELINE north_star gather roofline: t_roof = U/BW_HBM + G/BW_L2; "
                               "achieved = G / gather time, peak = G / t_roof (frac = t_roof/t)",
                 "gathered_bytes_G": int(G),
