@@ -150,3 +150,24 @@ def test_sharded_two_ranks(mode, combine, chunks, hash_mode, h, n):
         assert err < 2e-6, (rank, err)
         if mode == "table" and combine == "reduce_scatter":
             assert shape == (n // 2, 32)
+
+
+@pytest.mark.parametrize("combine", ["all_reduce", "none"])
+def test_sharded_three_ranks_token_hash(combine):
+    """World 3 over gloo: h = 11 tables split 4 / 4 / 3 and n = 25 tokens split
+    9 / 8 / 8 -- every all-to-all split size differs from its neighbours."""
+    world, h, n = 3, 11, 25
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, "table", combine, 1, q, "token", h, n))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    results = sorted(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert [r[1] for r in results] == [(0, 4), (4, 8), (8, 11)]
+    for rank, _, shape, err in results:
+        assert err < 2e-6, (rank, err)
