@@ -152,11 +152,12 @@ def test_sharded_two_ranks(mode, combine, chunks, hash_mode, h, n):
             assert shape == (n // 2, 32)
 
 
-@pytest.mark.parametrize("combine", ["all_reduce", "none"])
-def test_sharded_three_ranks_token_hash(combine):
+@pytest.mark.parametrize("combine,n", [("all_reduce", 25), ("none", 25), ("reduce_scatter", 24)])
+def test_sharded_three_ranks_token_hash(combine, n):
     """World 3 over gloo: h = 11 tables split 4 / 4 / 3 and n = 25 tokens split
-    9 / 8 / 8 -- every all-to-all split size differs from its neighbours."""
-    world, h, n = 3, 11, 25
+    9 / 8 / 8 -- every all-to-all split size differs from its neighbours
+    (reduce-scatter needs n divisible by the world: 24)."""
+    world, h = 3, 11
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
