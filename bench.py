@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--hash-mode", default="token", choices=["token", "replicated"],
                     help="table sharding: hash the rank's own token block and all-to-all the "
                          "records (token), or recompute the full hash on every rank")
+    ap.add_argument("--table-sharded", type=int, default=-1,
+                    help="also measure c3 (reduce-scatter) and c4 (all-reduce) table-sharded "
+                         "and report them under 'table_sharded' (default: at N > 1)")
     ap.add_argument("--shard", default="auto", choices=["auto", "token", "table"],
                     help="N>1 partitioning: token (tables replicated, c1/c2/c5) or table "
                          "(tables split over ranks, partials combined by NCCL; c3/c4); "
@@ -403,6 +406,7 @@ def run_ours(args):
         e2e_mean = float(t.item())
 
     result = None
+    l2 = 0.0
     if rank == 0:
         peaks, peak_src = load_peaks()
         hbm = float(peaks.get("hbm_gbs", 6650.0))
@@ -424,6 +428,7 @@ def run_ours(args):
         tokens_total = n * world if mode == "token" else n
         value = tokens_total / (mean_ms * 1e-3)
         traffic = load_traffic(args.config, args.kind)
+        t_fwd = mean_ms
         result = {
             "metric": METRIC,
             "value": round(value, 1),
@@ -461,24 +466,34 @@ def run_ours(args):
             "gpu_launches": int(launches),
             "stages_ms": {"hash": round(hash_avg, 5), "gather": round(gather_avg, 5)},
             "roofline": {
-                "bound": "hbm",
+                # memory-bound: t_roof = U/BW_HBM + G/BW_L2, and the L2 term
+                # dominates (c2: 94 %) -- the bound is the L2 -> SM read path
+                "bound": "l2",
                 "kernel": "gather_accumulate",
                 "achieved": round(achieved, 1),
                 "peak": round(peak_eff, 1),
                 "unit": "GB/s",
                 "frac": round(achieved / peak_eff, 4),
+                # the whole forward (hash + gather) on the same roofline: the
+                # north star's "tokens/s as achieved fraction of the memory
+                # roofline"
+                "frac_forward": round(t_roof_ms / t_fwd, 4),
                 # dram__bytes_read.sum + dram__bytes_write.sum of the gather
                 # launch, bytes, from the committed ncu --set full capture
                 "traffic": (traffic or {}).get("dram_bytes_per_launch"),
                 "traffic_source": (traffic or {}).get("source"),
                 "definition": "BASELINE north_star gather roofline: t_roof = U/BW_HBM + G/BW_L2; "
-                              "achieved = G / gather time, peak = G / t_roof (frac = t_roof/t)",
+                              "achieved = G / gather time, peak = G / t_roof (frac = t_roof / "
+                              "t_gather); frac_forward = t_roof / ms_per_step",
                 "gathered_bytes_G": int(G),
                 "unique_bytes_U": int(U),
                 "bw_hbm_gbs": hbm,
                 "bw_hbm_source": peak_src + " MEASURED_PEAKS.json hbm_gbs",
                 "bw_l2_gbs": round(l2, 1),
-                "bw_l2_source": "measured live (lffn_probe_bandwidth, 32 MiB re-read)",
+                "bw_l2_source": "measured live, the best L2 read rate found on B200: 128-bit "
+                                "sequential re-reads of a 32 MiB buffer from every SM "
+                                "(lffn_probe_bandwidth 0; cross-checked with ncu in "
+                                "profiles/r2_l2_probe.md)",
                 "t_roof_ms": round(t_roof_ms, 5),
                 # context, not the denominator: the same probe with the
                 # gather's access pattern (random 512-byte segments)
@@ -494,37 +509,229 @@ def run_ours(args):
         }
         if small is not None:
             result["small_batch_latency"] = small
+    want_ts = args.table_sharded if args.table_sharded >= 0 else int(world > 1)
+    if want_ts and mode == "token" and args.config not in ("c3", "c4"):
+        # BASELINE's table-sharded configs on the same ranks (north star:
+        # c3 reduce-scatter, c4 all-reduce at 1 / 2 / 4 / 8 GPUs)
+        layer.close()
+        del xd, yd, flush
+        torch.cuda.empty_cache()
+        if dist is None:
+            import socket
+
+            import torch.distributed as dist
+
+            with socket.socket() as sk:
+                sk.bind(("127.0.0.1", 0))
+                port = sk.getsockname()[1]
+            dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0,
+                                    world_size=1, device_id=torch.device("cuda", local))
+        l2b = torch.tensor([l2 if rank == 0 else 0.0], device="cuda")
+        dist.all_reduce(l2b, op=dist.ReduceOp.MAX)
+        hbm_b = float(load_peaks()[0].get("hbm_gbs", 6650.0))
+        ts = {}
+        for name, comb in (("c3", "reduce_scatter"), ("c4", "all_reduce")):
+            try:
+                ts[name] = table_sharded_measure(name, comb, rank, world, local,
+                                                 max(3, args.steps // 2), 3,
+                                                 float(l2b.item()), hbm_b)
+            except Exception as e:  # reported, never fatal for the headline line
+                ts[name] = {"error": f"{type(e).__name__}: {str(e)[:300]}"}
+        if result is not None:
+            result["table_sharded"] = ts
+        layer = None
     if dist:
         dist.barrier()
         dist.destroy_process_group()
     if sharded is not None:
         sharded.close()
-    else:
+    elif layer is not None:
         layer.close()
     return result
 
 
+# ----------------------------------------------------------- table sharding
+def table_sharded_measure(name: str, combine: str, rank: int, world: int, local: int,
+                          steps: int, warmup: int, l2_gbs: float, hbm_gbs: float):
+    """BASELINE's table-sharded configs (c3: NCCL reduce-scatter, c4: NCCL
+    all-reduce): every rank owns tables split_range(h, P, r) -- built as a
+    slice of the reference-seeded stack, never the whole stack -- hashes its
+    own token block for all tables, receives the records of its tables by one
+    all-to-all, gathers the fp32 partial for all n tokens and the partials
+    are combined chunk by chunk (sharded.py).  Reported: tokens/s (max over
+    ranks), the compute alone (hash + gather of the rank) on its own roofline
+    (U/P at HBM + G/P at L2), and the combine alone against its bus bytes."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2403_07221_b200 import Projection
+    from paper_2403_07221_b200.configs import (WORKLOADS, config_of, make_table_slice, make_x,
+                                               spec_of)
+    from paper_2403_07221_b200.flops import unique_table_bytes
+    from paper_2403_07221_b200.sharded import ShardedLookupFFN, split_range
+
+    w = WORKLOADS[name]
+    cfg = config_of(w)
+    proj = Projection.init(spec_of(w), 1)
+    kb, ke = split_range(w.h, world, rank)
+    chunks = 4
+    q = world * chunks
+    n = ((w.n + q - 1) // q) * q
+    T = make_table_slice(w, kb, ke)
+    sh = ShardedLookupFFN(cfg, proj, T, mode="table", combine=combine, device=local,
+                          max_tokens=n, table_dtype=w.table_dtype, chunks=chunks)
+    del T
+    x = make_x(w, n, seed=0)
+    xd = torch.from_numpy(x).cuda()
+    d = cfg.d_out
+    y = torch.empty((n // world if combine == "reduce_scatter" else n, d), dtype=torch.float32,
+                    device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def timed(fn, reps, pre=None):
+        out = []
+        for i in range(reps):
+            if pre:
+                pre(i)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            out.append((e0, e1))
+        torch.cuda.synchronize()
+        return [a.elapsed_time(b) for a, b in out]
+
+    def maxr(v):
+        t = torch.tensor([float(v)], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for i in range(warmup):
+        flush.fill_(i & 0xFF)
+        sh.forward(xd, y)
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    step = maxr(np.mean(timed(lambda: sh.forward(xd, y), steps,
+                              pre=lambda i: flush.fill_(i & 0xFF))))
+    # the rank's compute alone: hash of its token block, gather of its tables
+    t0, t1 = split_range(n, world, rank)
+    codes, coeff = sh.exchange_records(xd)
+    torch.cuda.synchronize()
+    part = torch.empty((n, d), dtype=torch.float32, device="cuda")
+    reps = max(3, steps // 2)
+    hash_ms = maxr(np.mean(timed(lambda: sh.hasher.hash(xd[t0:t1]), reps,
+                                 pre=lambda i: flush.fill_(i & 0xFF))))
+    gather_ms = maxr(np.mean(timed(lambda: sh.layer.lookup_accumulate(codes, coeff, part), reps,
+                                   pre=lambda i: flush.fill_(i & 0xFF))))
+    # the combine alone, on the full partial
+    if combine == "reduce_scatter":
+        out = torch.empty((n // world, d), dtype=torch.float32, device="cuda")
+        comm = lambda: dist.reduce_scatter_tensor(out, part)  # noqa: E731
+        bus = (world - 1) / world * n * d * 4
+    else:
+        comm = lambda: dist.all_reduce(part)  # noqa: E731
+        bus = 2 * (world - 1) / world * n * d * 4
+    comm()
+    torch.cuda.synchronize()
+    dist.barrier()
+    comm_ms = maxr(np.mean(timed(comm, reps)))
+    elem = 4 if w.table_dtype == "f32" else 2
+    U = unique_table_bytes(codes.cpu().numpy().view(np.uint32), cfg, elem)
+    G = n * (ke - kb) * d * elem
+    t_roof = (U / (hbm_gbs * 1e9) + G / (l2_gbs * 1e9)) * 1e3
+    sh.close()
+    del xd, y, part, flush
+    torch.cuda.empty_cache()
+    return {
+        "config": f"{w.name}: d={w.d} h={w.h} tau={w.tau} n={n} {w.table_dtype} tables, "
+                  f"tables split over {world} ranks, hash of each rank's token block + "
+                  f"all-to-all of the records, NCCL {combine} of the fp32 partials in "
+                  f"{chunks} chunks overlapped with the gather",
+        "tokens_per_s": round(n / (step * 1e-3), 1),
+        "ms_per_step": round(step, 4),
+        "scaling": "strong",
+        "compute_ms": {"hash_rank_block": round(hash_ms, 4), "gather_rank_tables": round(gather_ms, 4)},
+        "compute_roofline": {"t_roof_ms": round(t_roof, 5),
+                             "frac": round(t_roof / (hash_ms + gather_ms), 4),
+                             "frac_gather": round(t_roof / gather_ms, 4),
+                             "unique_bytes_U_rank0": int(U), "gathered_bytes_G_rank": int(G),
+                             "definition": "U/P at BW_HBM + G/P at BW_L2 (rank 0's slice)"},
+        "combine": {"op": combine, "ms": round(comm_ms, 4), "bus_bytes": int(bus),
+                    "bus_gbs": round(bus / (comm_ms * 1e-3) / 1e9, 1) if world > 1 else None},
+    }
+
+
 # ---------------------------------------------------------------- reference
-def reference_sample(args, w, n_sample, threads, reps):
-    """Time the reference's float32 inference kernels on host cores."""
-    from oracle import Reference, Spec, Cfg
-    from paper_2403_07221_b200 import ProjKind
-    from paper_2403_07221_b200.configs import make_params, make_x
+def reference_inputs(w, kind_name: str, n: int, ref):
+    """x, projection blob and tables of workload w built by the REFERENCE
+    library itself (oracle/_ref/liblffn_ref.so: make_rng + fill_gaussian,
+    Projection::init), with the bench's seeds -- the values are bit-identical
+    to the ours arm's (tests/test_oracle_pin.py), but no code of this
+    repository's product library runs on the reference arm."""
+    from oracle import Spec
+    from paper_2403_07221_b200.configs import TABLE_STD, make_x, spec_of
+    from paper_2403_07221_b200.lookup import ProjKind
+
+    sp = spec_of(w, ProjKind[kind_name])
+    s = Spec(sp.d_in, sp.d_out, int(sp.kind), sp.stages, sp.block, sp.depth)
+    x = make_x(w, n, gaussian=lambda seed, cnt: ref.gaussian(seed, cnt))
+    blob = ref.proj_init(s, 1)
+    T = ref.gaussian(2, w.h * (1 << w.tau) * w.d, TABLE_STD)
+    return s, x, blob, T
+
+
+def reference_measure(args, w, steps: int, warmup: int, cores: int):
+    """The reference's float32 inference pipeline (lookup_hash_f32 ->
+    lookup_weights_f32 -> lookup_gather_f32 | lookup_gather_sorted_f32,
+    bench.cpp:115-217, compiled from the reference sources) over the
+    workload's FULL batch on `cores` host threads (256-row tiles, one per
+    thread at a time).  The faster of the plain and the sorted ("opt1")
+    gather is timed; the float64 lookup_forward (lookup.cpp:279-282) and the
+    single-core rate are reported beside it on bounded samples."""
+    from oracle import Cfg, Reference
 
     ref = Reference()
-    kind = ProjKind[args.kind]
-    cfg, proj, T = make_params(w, kind)
-    x = make_x(w, n_sample)
-    c = Cfg(cfg.d_in, cfg.d_out, cfg.tables, cfg.code_bits)
-    s = Spec(proj.spec.d_in, proj.spec.d_out, int(kind))
-    blob32 = proj.blob.astype(np.float32)
-    T32 = T.data.astype(np.float32)
-    del T
-    times = []
-    for _ in range(reps):
-        _, ms = ref.pipeline_f32(c, s, blob32, T32, x, threads=threads, reps=1)
-        times.append(ms)
-    return times
+    n = w.n
+    s, x, blob, T = reference_inputs(w, args.kind, n, ref)
+    c = Cfg(w.d, w.d, w.h, w.tau)
+    blob32 = blob.astype(np.float32)
+    T32 = T.astype(np.float32)
+    # a warm-up pass (first touch of the buffers), then one pass of each
+    # gather variant picks the faster one
+    ref.pipeline_f32(c, s, blob32, T32, x, threads=cores, reps=1)
+    variants = {}
+    for sg in (False, True):
+        _, ms = ref.pipeline_f32(c, s, blob32, T32, x, threads=cores, sorted_gather=sg, reps=1)
+        variants["sorted" if sg else "plain"] = ms
+    best = min(variants, key=variants.get)
+    sg = best == "sorted"
+    for _ in range(max(0, warmup - 1)):
+        ref.pipeline_f32(c, s, blob32, T32, x, threads=cores, sorted_gather=sg, reps=1)
+    times = [ref.pipeline_f32(c, s, blob32, T32, x, threads=cores, sorted_gather=sg, reps=1)[1]
+             for _ in range(steps)]
+    ms = float(np.mean(times))
+    # single core, plain gather, 1024 tokens
+    n1 = min(n, 1024)
+    _, t1 = ref.pipeline_f32(c, s, blob32, T32, x[:n1], threads=1, reps=1)
+    # float64 lookup_forward (the reference's verification path: OpenMP
+    # projection, serial gather) on 256 tokens
+    n64 = min(n, 256)
+    t0 = time.perf_counter()
+    ref.lookup_forward(c, s, blob, T, x[:n64].astype(np.float64))
+    t64 = (time.perf_counter() - t0) * 1e3
+    return {
+        "ms": ms, "n": n, "gather": best,
+        "variants_tokens_per_s": {k: round(n / (v * 1e-3), 1) for k, v in variants.items()},
+        "single_core_tokens_per_s": round(n1 / (t1 * 1e-3), 1),
+        "f64_lookup_forward_tokens_per_s": round(n64 / (t64 * 1e-3), 1),
+        "sample": (f"the full {n}-token batch of {w.name} per step through the reference f32 "
+                   f"kernels (bench.cpp:115-217, {best} gather, the faster of plain / sorted), "
+                   f"256-row tiles over {cores} OpenMP threads; inputs built by the reference "
+                   f"library (liblffn_ref.so); {cpu_model()}"),
+    }
 
 
 def run_reference(args):
@@ -535,12 +742,8 @@ def run_reference(args):
 
     w = WORKLOADS[args.config]
     cores = host_cores()
-    n_sample = args.cpu_sample or min(w.n, 4096)
-    for _ in range(args.warmup):
-        pass
-    times = reference_sample(args, w, n_sample, cores, args.warmup + args.steps)[args.warmup:]
-    ms = float(np.mean(times))
-    value = n_sample / (ms * 1e-3)
+    m = reference_measure(args, w, args.steps, args.warmup, cores)
+    value = m["n"] / (m["ms"] * 1e-3)
     return {
         "impl": "reference",
         "metric": METRIC,
@@ -549,44 +752,58 @@ def run_reference(args):
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": round(ms, 3),
+        "ms_per_step": round(m["ms"], 3),
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f32",
-        "data": "synthetic (same seeds as the ours arm)",
-        "config": {"workload": f"{w.name}: d_in=d_out={w.d} h={w.h} tau={w.tau} {args.kind}; "
-                               f"each step a {n_sample}-token sample",
-                   "tokens_per_step": n_sample},
+        "data": "synthetic (same seeds as the ours arm, generated by the reference library)",
+        "config": {"workload": f"{w.name}: d_in=d_out={w.d} h={w.h} tau={w.tau} n={w.n} "
+                               f"{args.kind} f32 tables (the reference f32 pipeline)",
+                   "tokens_per_step": m["n"]},
         "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": cores,
-                         "kind": "reference",
-                         "sample": f"{n_sample} tokens/step of {w.name}; reference f32 kernels "
-                                   "(bench.cpp:115-217) over 256-row tiles spread on "
-                                   f"{cores} OpenMP threads; {cpu_model()}"},
+                         "kind": "reference", "sample": m["sample"],
+                         "gather_variants_tokens_per_s": m["variants_tokens_per_s"],
+                         "single_core_tokens_per_s": m["single_core_tokens_per_s"],
+                         "f64_lookup_forward_tokens_per_s": m["f64_lookup_forward_tokens_per_s"]},
         "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
 
 
 def cpu_baseline_for(args):
-    """cpu_baseline of the ours line: the reference on a bounded sample."""
+    """cpu_baseline of the ours line: the same measurement as the reference
+    arm (full batch, all host cores, faster gather variant), fewer steps."""
     from paper_2403_07221_b200.configs import WORKLOADS
 
     w = WORKLOADS[args.config]
     cores = host_cores()
-    n_sample = min(w.n, 8192)
-    times = reference_sample(args, w, n_sample, cores, 2)
-    ms = min(times)
-    t1 = reference_sample(args, w, min(w.n, 1024), 1, 1)[0]
-    return {"value": round(n_sample / (ms * 1e-3), 1), "unit": UNIT, "cores": cores,
-            "kind": "reference",
-            "sample": f"{n_sample} tokens of {w.name} through the reference f32 kernels "
-                      f"(bench.cpp:115-217), 256-row tiles on {cores} threads; {cpu_model()}",
-            "single_core_tokens_per_s": round(min(w.n, 1024) / (t1 * 1e-3), 1)}
+    m = reference_measure(args, w, 3, 1, cores)
+    return {"value": round(m["n"] / (m["ms"] * 1e-3), 1), "unit": UNIT, "cores": cores,
+            "kind": "reference", "sample": m["sample"],
+            "gather_variants_tokens_per_s": m["variants_tokens_per_s"],
+            "single_core_tokens_per_s": m["single_core_tokens_per_s"],
+            "f64_lookup_forward_tokens_per_s": m["f64_lookup_forward_tokens_per_s"]}
+
+
+def relaunch(args) -> int:
+    """--gpus N > 1 without a torchrun environment: launch N ranks the way the
+    driver does (torch.distributed.run, one process per GPU, 127.0.0.1)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port",
+           str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
 
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
     if args.impl == "reference":
         out = run_reference(args)
         if out is not None:

@@ -103,6 +103,10 @@ int64_t lffn_proj_blob_size(const lffn_proj* proj);
 int lffn_proj_init(const lffn_proj* spec, uint64_t seed, double* blob_out);
 /* make_rng(seed) + fill_gaussian / fill_signs (common.hpp:44-55) */
 int lffn_fill_gaussian(uint64_t seed, double* out, int64_t n, double stddev);
+/* Elements [skip, skip + n) of the same make_rng(seed) + fill_gaussian stream
+ * (one distribution object over the whole stream, the first `skip` draws
+ * discarded): a table shard's slice of HashTables data without the rest. */
+int lffn_fill_gaussian_slice(uint64_t seed, int64_t skip, double* out, int64_t n, double stddev);
 int lffn_fill_signs(uint64_t seed, double* out, int64_t n);
 /* HashTables::init (lookup.cpp:39-49): std 1/sqrt(h) */
 int lffn_tables_init(const lffn_cfg* cfg, uint64_t seed, double* out);
@@ -134,6 +138,10 @@ int lffn_ctx_table_range(const lffn_ctx* ctx, int64_t* begin, int64_t* end);
  * store_dtype (LFFN_F32 or LFFN_BF16) and a shard keeps only its slice.
  * Tables are read-only afterwards (lookup.hpp:41-42). */
 int lffn_tables_upload(lffn_ctx* ctx, const void* host_T, int host_dtype, int store_dtype);
+/* The same upload from a host buffer holding only this context's slice
+ * [table_end-table_begin][2^tau][d_out] (a table shard built without the
+ * rest of the stack, e.g. by lffn_fill_gaussian_slice). */
+int lffn_tables_upload_slice(lffn_ctx* ctx, const void* host_slice, int host_dtype, int store_dtype);
 /* Use a caller-owned device buffer holding this context's slice
  * [table_end-table_begin][2^tau][d_out] in dtype (no copy). */
 int lffn_tables_attach(lffn_ctx* ctx, const void* d_T, int dtype);

@@ -17,8 +17,10 @@ from .lookup import (
     Projection,
     ProjectionSpec,
     ProjKind,
+    TableSlice,
     checkpoint_header,
     fill_gaussian,
+    fill_gaussian_slice,
     fill_signs,
     gaussian_matrix,
     load_checkpoint,
@@ -29,6 +31,6 @@ from .lookup import (
 
 __all__ = [
     "HashTables", "LookupConfig", "LookupFFN", "LookupVariant", "Projection", "ProjectionSpec",
-    "ProjKind", "fill_gaussian", "fill_signs", "gaussian_matrix", "lookup_forward",
+    "ProjKind", "TableSlice", "fill_gaussian", "fill_gaussian_slice", "fill_signs", "gaussian_matrix", "lookup_forward",
     "to_bf16_values", "flops", "checkpoint_header", "load_checkpoint", "save_checkpoint", "LffnError", "NumericError", "SizeError", "UsageError",
 ]

@@ -42,6 +42,7 @@ SIGNATURES = {
     "lffn_proj_blob_size": (_I64, [C.POINTER(lffn_proj)]),
     "lffn_proj_init": (C.c_int, [C.POINTER(lffn_proj), C.c_uint64, _VP]),
     "lffn_fill_gaussian": (C.c_int, [C.c_uint64, _VP, _I64, C.c_double]),
+    "lffn_fill_gaussian_slice": (C.c_int, [C.c_uint64, _I64, _VP, _I64, C.c_double]),
     "lffn_fill_signs": (C.c_int, [C.c_uint64, _VP, _I64]),
     "lffn_tables_init": (C.c_int, [C.POINTER(lffn_cfg), C.c_uint64, _VP]),
     "lffn_convert": (C.c_int, [_VP, C.c_int, _VP, C.c_int, _I64]),
@@ -58,6 +59,7 @@ SIGNATURES = {
     "lffn_ctx_destroy": (C.c_int, [_VP]),
     "lffn_ctx_table_range": (C.c_int, [_VP, C.POINTER(_I64), C.POINTER(_I64)]),
     "lffn_tables_upload": (C.c_int, [_VP, _VP, C.c_int, C.c_int]),
+    "lffn_tables_upload_slice": (C.c_int, [_VP, _VP, C.c_int, C.c_int]),
     "lffn_tables_attach": (C.c_int, [_VP, _VP, C.c_int]),
     "lffn_hash": (C.c_int, [_VP, _VP, _I64, _VP, _VP, _VP, _VP]),
     "lffn_lookup_accumulate": (C.c_int, [_VP, _VP, _VP, _I64, _VP, C.c_int, _VP]),

@@ -15,7 +15,7 @@ from typing import Optional
 import numpy as np
 
 from .lookup import (HashTables, LookupConfig, Projection, ProjectionSpec, ProjKind,
-                     fill_gaussian)
+                     TableSlice, fill_gaussian, fill_gaussian_slice)
 
 TABLE_STD = 0.02
 
@@ -57,19 +57,22 @@ def spec_of(w: Workload, kind: ProjKind = ProjKind.signflip) -> ProjectionSpec:
     return ProjectionSpec(w.d, w.h * w.tau, kind)
 
 
-def make_x(w: Workload, n: Optional[int] = None, seed: int = 0) -> np.ndarray:
-    """Token inputs, float32 [n x d]."""
+def make_x(w: Workload, n: Optional[int] = None, seed: int = 0, gaussian=None) -> np.ndarray:
+    """Token inputs, float32 [n x d].  ``gaussian(seed, count)`` draws the
+    make_rng(seed) stream (default: this package's bit-identical restatement;
+    the bench's reference arm passes the reference library's own)."""
     n = w.n if n is None else n
+    fill = fill_gaussian if gaussian is None else gaussian
     if w.x_kind == "skew":
         # x = U z + 0.01 eps: U ~ N(0,1) 768x4 from make_rng(seed); per token
         # z ~ N(0,1)^4 then eps ~ N(0,1)^d from make_rng(seed + 100).  Both
         # per-token draws have even length, so one continuing fill equals
         # the per-token fills.
-        U = fill_gaussian(seed, w.d * 4).reshape(w.d, 4)
-        draws = fill_gaussian(seed + 100, n * (4 + w.d)).reshape(n, 4 + w.d)
+        U = fill(seed, w.d * 4).reshape(w.d, 4)
+        draws = fill(seed + 100, n * (4 + w.d)).reshape(n, 4 + w.d)
         x = draws[:, :4] @ U.T + 0.01 * draws[:, 4:]
         return np.ascontiguousarray(x, np.float32)
-    x = fill_gaussian(seed, n * w.d).reshape(n, w.d)
+    x = fill(seed, n * w.d).reshape(n, w.d)
     if w.x_kind == "standardized":
         mu = x.mean(axis=1, keepdims=True)
         sd = x.std(axis=1, keepdims=True)
@@ -83,3 +86,12 @@ def make_params(w: Workload, kind: ProjKind = ProjKind.signflip, seed: int = 0):
     proj = Projection.init(spec_of(w, kind), seed + 1)
     data = fill_gaussian(seed + 2, w.h * (1 << w.tau) * w.d, TABLE_STD)
     return cfg, proj, HashTables(w.h, w.tau, w.d, data)
+
+
+def make_table_slice(w: Workload, kb: int, ke: int, seed: int = 0) -> TableSlice:
+    """Tables [kb, ke) of make_params' stack (the same make_rng(seed+2) stream,
+    the prefix drawn and discarded) without materialising the whole stack --
+    what a table shard of c4 (4.3 GB of float64 tables) uploads."""
+    per = (1 << w.tau) * w.d
+    data = fill_gaussian_slice(seed + 2, kb * per, (ke - kb) * per, TABLE_STD)
+    return TableSlice((kb, ke), w.tau, w.d, data)

@@ -180,6 +180,15 @@ int lffn_fill_gaussian(uint64_t seed, double* out, int64_t n, double stddev) {
   return LFFN_OK;
 }
 
+int lffn_fill_gaussian_slice(uint64_t seed, int64_t skip, double* out, int64_t n, double stddev) {
+  if (!out || n < 0 || skip < 0) return fail(LFFN_ERR_USAGE, "fill_gaussian_slice: bad arguments");
+  std::mt19937_64 rng(seed);
+  std::normal_distribution<double> dist(0.0, stddev);
+  for (int64_t i = 0; i < skip; ++i) (void)dist(rng);
+  for (int64_t i = 0; i < n; ++i) out[i] = dist(rng);
+  return LFFN_OK;
+}
+
 int lffn_fill_signs(uint64_t seed, double* out, int64_t n) {
   if (!out || n < 0) return fail(LFFN_ERR_USAGE, "fill_signs: bad arguments");
   std::mt19937_64 rng(seed);

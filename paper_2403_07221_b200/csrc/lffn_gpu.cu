@@ -1173,6 +1173,20 @@ int lffn_tables_upload(lffn_ctx* c, const void* host_T, int host_dtype, int stor
   return LFFN_OK;
 }
 
+int lffn_tables_upload_slice(lffn_ctx* c, const void* host_slice, int host_dtype, int store_dtype) {
+  if (!c || !host_slice) return fail(LFFN_ERR_USAGE, "tables upload: null argument");
+  const size_t per_table = size_t(c->rows) * size_t(c->cfg.d_out);
+  const size_t hsz = host_dtype == LFFN_F64 ? 8 : host_dtype == LFFN_F32 ? 4 : 2;
+  const int64_t chunk = std::max<int64_t>(1, int64_t((size_t(64) << 20) / (per_table * hsz)));
+  for (int64_t k0 = 0; k0 < c->h_loc; k0 += chunk) {
+    const int64_t nk = std::min(chunk, c->h_loc - k0);
+    if (int rc = tables_upload_range(c, static_cast<const char*>(host_slice) + size_t(k0) * per_table * hsz,
+                                     host_dtype, store_dtype, k0, nk))
+      return rc;
+  }
+  return LFFN_OK;
+}
+
 int lffn_convert(const void* src, int src_dtype, void* dst, int dst_dtype, int64_t n) {
   if ((!src || !dst) && n > 0) return fail(LFFN_ERR_USAGE, "convert: null buffer");
   for (int64_t i = 0; i < n; ++i) {

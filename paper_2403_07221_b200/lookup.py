@@ -203,6 +203,24 @@ class HashTables:
         return h
 
 
+@dataclass
+class TableSlice:
+    """Tables [kb, ke) of a stack, float64 host copy: what a table shard
+    uploads (``LookupFFN(..., table_range=(kb, ke))``)."""
+
+    table_range: tuple
+    code_bits: int
+    d_out: int
+    data: np.ndarray = field(repr=False)
+
+
+def fill_gaussian_slice(seed: int, skip: int, n: int, stddev: float = 1.0) -> np.ndarray:
+    """Elements [skip, skip + n) of make_rng(seed) + fill_gaussian."""
+    out = np.empty(n, np.float64)
+    check(_capi.lib().lffn_fill_gaussian_slice(seed, skip, out.ctypes.data, n, stddev))
+    return out
+
+
 def fill_gaussian(seed: int, n: int, stddev: float = 1.0) -> np.ndarray:
     """make_rng(seed) + fill_gaussian (common.hpp:44-49), bit-identical."""
     out = np.empty(n, np.float64)
@@ -310,8 +328,15 @@ class LookupFFN:
         if hasattr(data, "detach"):
             data = data.detach().cpu().numpy()
         data = np.ascontiguousarray(data)
-        expect = self.cfg.tables * self.cfg.table_rows() * self.cfg.d_out
-        if data.size != expect:
+        per_table = self.cfg.table_rows() * self.cfg.d_out
+        expect = self.cfg.tables * per_table
+        kb, ke = self.table_range
+        sliced = isinstance(tables, TableSlice) or (data.size != expect and
+                                                    data.size == (ke - kb) * per_table)
+        if sliced and (data.size != (ke - kb) * per_table or
+                       (isinstance(tables, TableSlice) and tables.table_range != (kb, ke))):
+            raise SizeError("lookup forward: table slice does not match the layer's table range")
+        if not sliced and data.size != expect:
             raise SizeError("lookup forward: table stack shape mismatch")
         if data.dtype == np.float64:
             host = LFFN_F64
@@ -321,7 +346,8 @@ class LookupFFN:
             host = LFFN_BF16
         else:
             raise UsageError(f"unsupported table dtype {data.dtype}")
-        check(_capi.lib().lffn_tables_upload(self._ctx, data.ctypes.data, host, self.table_dtype))
+        up = _capi.lib().lffn_tables_upload_slice if sliced else _capi.lib().lffn_tables_upload
+        check(up(self._ctx, data.ctypes.data, host, self.table_dtype))
 
     def attach_tables(self, dev_tensor) -> None:
         """Use a caller-owned device tensor holding this shard's slice (no copy)."""
