@@ -643,7 +643,33 @@ def table_sharded_measure(name: str, combine: str, rank: int, world: int, local:
     G = n * (ke - kb) * d * elem
     t_roof = (U / (hbm_gbs * 1e9) + G / (l2_gbs * 1e9)) * 1e3
     sh.close()
-    del xd, y, part, flush
+    del part
+    torch.cuda.empty_cache()
+    # the same forward through the C-ABI group (lffn_forward_sharded: NCCL
+    # owned by the library, no torch on the data path)
+    native = None
+    try:
+        from paper_2403_07221_b200.sharded import NativeTableShard
+
+        ids = [NativeTableShard.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(ids, src=0)
+        T = make_table_slice(w, kb, ke)
+        ng = NativeTableShard(cfg, proj, T, rank=rank, world=world, nccl_id=ids[0],
+                              device=local, max_tokens=n, table_dtype=w.table_dtype,
+                              chunks=chunks)
+        del T
+        for i in range(warmup):
+            ng.forward(xd, y, combine=combine)
+        torch.cuda.synchronize()
+        dist.barrier()
+        nstep = maxr(np.mean(timed(lambda: ng.forward(xd, y, combine=combine), steps,
+                                   pre=lambda i: flush.fill_(i & 0xFF))))
+        native = {"tokens_per_s": round(n / (nstep * 1e-3), 1), "ms_per_step": round(nstep, 4),
+                  "path": "lffn_group / lffn_forward_sharded (C-ABI, NCCL owned by the group)"}
+        ng.close()
+    except Exception as e:  # reported, never fatal
+        native = {"error": f"{type(e).__name__}: {str(e)[:300]}"}
+    del xd, y, flush
     torch.cuda.empty_cache()
     return {
         "config": f"{w.name}: d={w.d} h={w.h} tau={w.tau} n={n} {w.table_dtype} tables, "
@@ -661,6 +687,7 @@ def table_sharded_measure(name: str, combine: str, rank: int, world: int, local:
                              "definition": "U/P at BW_HBM + G/P at BW_L2 (rank 0's slice)"},
         "combine": {"op": combine, "ms": round(comm_ms, 4), "bus_bytes": int(bus),
                     "bus_gbs": round(bus / (comm_ms * 1e-3) / 1e9, 1) if world > 1 else None},
+        "native_group": native,
     }
 
 

@@ -229,21 +229,64 @@ int lffn_sync(lffn_ctx* ctx, void* stream);
  *                              than the resident warp slots split each
  *                              token's table walk over 2-8 warps), -1 = one
  *                              warp per token (part) always
- *   LFFN_OPT_FUSED             0 (default) = hash kernel, then gather kernel;
- *                              1 = both in one warp-specialised persistent
- *                              kernel where the shape allows (signflip,
- *                              D = 2048; measured slower, for A/B)
  *   LFFN_OPT_BF16_COEFF_FMA    1 (default) = bf16 tables: groups of tables
  *                              whose coefficients are bf16 values (e.g. the
  *                              top-1 weight 1.0) accumulate with the exact
  *                              mixed-precision FMA on the packed halves (bit-
- *                              identical to the fp32 FMA); 0 = always unpack */
+ *                              identical to the fp32 FMA); 0 = always unpack
+ *   LFFN_OPT_BWD_ONE_PASS      1 = the backward's single-pass table-row dot
+ *                              (the A/B reference of the default two passes)
+ *   LFFN_OPT_HASH_EXACT        1 = the signflip hash always runs the stage
+ *                              order of fwht_kernel (z bit-identical); 0
+ *                              (default) = the production kernel at D = 2048 /
+ *                              4096 (reordered stages, codes bit-exact
+ *                              wherever |z| > 1e-5) unless z is requested
+ *   LFFN_OPT_HOST_CHUNKS       lffn_forward_host pipeline chunks (1 .. 16,
+ *                              default 8) */
 #define LFFN_OPT_DENSE_EXACT 1
 #define LFFN_OPT_TABLE_GROUP_BYTES 2
 #define LFFN_OPT_GATHER_VARIANT 3
-#define LFFN_OPT_FUSED 4
 #define LFFN_OPT_BF16_COEFF_FMA 5
+#define LFFN_OPT_BWD_ONE_PASS 6
+#define LFFN_OPT_HASH_EXACT 7
+#define LFFN_OPT_HOST_CHUNKS 8
 int lffn_ctx_set_option(lffn_ctx* ctx, int option, int64_t value);
+
+/* ---- multi-GPU table sharding (north star: tables split
+ * over GPUs, partial sums combined by NCCL reduce-scatter or all-reduce) ----
+ * One lffn_group per rank (one process per GPU).  The group owns an NCCL
+ * communicator (libnccl.so.2, loaded at run time), the rank's table shard
+ * (tables split_range(h, world, rank): the first h % world ranks own one
+ * more) and a table-less hash context for the rank's token block.
+ * lffn_forward_sharded(x = all n tokens, identical on every rank):
+ *   hash of the rank's token block for all tables, one grouped NCCL
+ *   send/recv exchange of the (code, coefficient) records (each rank
+ *   receives its tables' records for all n tokens), then per token chunk the
+ *   gather of the fp32 partial over the rank's tables and the combine on the
+ *   group's stream, overlapped with the next chunk's gather:
+ *     LFFN_COMBINE_REDUCE_SCATTER  y = rows [r n/P, (r+1) n/P) of the sum
+ *                                  (n a multiple of world * chunks)
+ *     LFFN_COMBINE_ALL_REDUCE      y = all n rows of the sum
+ *     LFFN_COMBINE_NONE            y = the rank's partial over its tables
+ * Stream-ordered on `stream`; returns after the non-finite check (like
+ * lffn_forward + lffn_sync). */
+typedef struct lffn_group lffn_group;
+#define LFFN_COMBINE_REDUCE_SCATTER 0
+#define LFFN_COMBINE_ALL_REDUCE 1
+#define LFFN_COMBINE_NONE 2
+/* ncclGetUniqueId into out[len >= 128]; rank 0 creates it and the ranks
+ * share it out of band (e.g. torch.distributed broadcast, MPI_Bcast). */
+int lffn_nccl_unique_id(void* out, int64_t len);
+int lffn_group_create(lffn_group** out, int device, int64_t max_tokens, const lffn_cfg* cfg,
+                      const lffn_proj* proj, const void* nccl_id, int rank, int world);
+int lffn_group_destroy(lffn_group* group);
+/* The rank's table shard: upload its tables with lffn_tables_upload(_slice)
+ * or lffn_tables_attach; set options on it. */
+lffn_ctx* lffn_group_shard(lffn_group* group);
+/* Token chunks of the gather / combine pipeline (1 .. 8, default 4). */
+int lffn_group_set_chunks(lffn_group* group, int chunks);
+int lffn_forward_sharded(lffn_group* group, const float* d_x, int64_t n, float* d_y, int combine,
+                         void* stream);
 
 /* Number of kernels launched through this context since creation. */
 int64_t lffn_ctx_launch_count(const lffn_ctx* ctx);

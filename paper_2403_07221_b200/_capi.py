@@ -16,8 +16,9 @@ LIB_PATH = os.path.join(HERE, "csrc", "liblffn_gpu.so")
 
 LFFN_OK, LFFN_ERR_USAGE, LFFN_ERR_NUMERIC, LFFN_ERR_RUNTIME = 0, 1, 2, 3
 LFFN_F32, LFFN_BF16, LFFN_F64 = 0, 1, 2
-LFFN_OPT_DENSE_EXACT, LFFN_OPT_TABLE_GROUP_BYTES, LFFN_OPT_GATHER_VARIANT, LFFN_OPT_FUSED = 1, 2, 3, 4
-LFFN_OPT_BF16_COEFF_FMA = 5
+LFFN_OPT_DENSE_EXACT, LFFN_OPT_TABLE_GROUP_BYTES, LFFN_OPT_GATHER_VARIANT = 1, 2, 3
+LFFN_OPT_BF16_COEFF_FMA, LFFN_OPT_BWD_ONE_PASS, LFFN_OPT_HASH_EXACT, LFFN_OPT_HOST_CHUNKS = 5, 6, 7, 8
+LFFN_COMBINE_REDUCE_SCATTER, LFFN_COMBINE_ALL_REDUCE, LFFN_COMBINE_NONE = 0, 1, 2
 
 
 class lffn_cfg(C.Structure):
@@ -75,6 +76,13 @@ SIGNATURES = {
     "lffn_probe_bandwidth": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]),
     "lffn_last_error": (C.c_char_p, []),
     "lffn_version": (C.c_char_p, []),
+    "lffn_nccl_unique_id": (C.c_int, [_VP, _I64]),
+    "lffn_group_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, _I64, C.POINTER(lffn_cfg),
+                                    C.POINTER(lffn_proj), _VP, C.c_int, C.c_int]),
+    "lffn_group_destroy": (C.c_int, [_VP]),
+    "lffn_group_shard": (_VP, [_VP]),
+    "lffn_group_set_chunks": (C.c_int, [_VP, C.c_int]),
+    "lffn_forward_sharded": (C.c_int, [_VP, _VP, _I64, _VP, C.c_int, _VP]),
 }
 
 _lib = None

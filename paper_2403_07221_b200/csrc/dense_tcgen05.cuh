@@ -54,11 +54,14 @@ struct DenseParams {
   uint32_t* codes;       // [n x hl]
   float* coeff;          // [n x hl]
   int* flag;
-  float fixup;           // |z| below this is recomputed exactly (kDenseFixup)
+  // |z| < fix_scale * ||x_t||_2 * ||w_c||_2 is recomputed exactly: a
+  // rigorous bound on the split-precision chain error (dense_fix_scale)
+  float fix_scale;
+  const float* xnorm;    // [n] ||x_t||_2 (rounded up), written by the x split
+  const float* wnorm;    // [ncols] ||W[:, c]||_2 of the slice (rounded up)
   uint2* fix_list;       // deferred exact recomputations {token, slice column}
   int* fix_count;        // entries appended (reset by dense_split_x_kernel)
   int fix_cap;           // capacity; a CTA that finds the list full fixes up inline
-  long long* prof;       // optional per-CTA timestamps (debug, LFFN_DENSE_PROF)
 };
 
 namespace umma {
@@ -138,10 +141,20 @@ __device__ __forceinline__ float tf32_rn(float f) {
 // The tensor core accumulates with truncation, so the error of a long MMA
 // chain grows linearly (3.2e-5 at c2 with one chain of 288 MMAs).  K is cut
 // into kSegs segments accumulated in separate TMEM columns and summed in fp32
-// round-to-nearest in the epilogue; z with |z| < kDenseFixup (far above the
-// remaining error) are recomputed exactly.
+// round-to-nearest in the epilogue.  Every accumulation step truncates by at
+// most 2^-23 of the running partial sum, which is bounded by
+// sum_k |x_k w_k| <= ||x||_2 ||w_c||_2 (Cauchy-Schwarz), and the operand
+// splits / the fp32 rounding of W add a few 2^-24 of the same sum, so
+// |z - z_exact| <= fix_scale * ||x||_2 * ||w_c||_2 with
+// fix_scale = (steps per segment + 48) * 2^-23 (dense_fix_scale); every z
+// inside that band is recomputed exactly, so the codes are bit-exact for any
+// input scale and width (c2: band ~6e-4 at ||x|| = 27.7, observed error
+// 1.7e-5).
 constexpr int kSegs = 2;
-constexpr float kDenseFixup = 1e-4f;
+inline float dense_fix_scale(int d_in) {
+  const int steps = ((d_in + 15) / 16) * 6 / kSegs + 48;
+  return float(steps) * 1.1920929e-7f;  // 2^-23
+}
 
 // tcgen05.ld 32x32b.xN: N consecutive TMEM columns of this thread's lane
 // (no wait; the caller issues tmem_wait_ld() once for a batch).
@@ -330,7 +343,6 @@ __global__ void __launch_bounds__(128, 2)
   const int nk = (p.d_in + BK - 1) / BK;
   const int nseg = nk < kSegs ? nk : kSegs;  // K segments actually written
   const int64_t cta = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
-  if (p.prof && tid == 0) p.prof[cta * 4] = globaltimer_ns();
 
   if (tid == 0) {
     // producer: stage kc reuses the slot of stage kc - kStages once its MMAs completed
@@ -385,7 +397,6 @@ __global__ void __launch_bounds__(128, 2)
   __syncwarp();
   mbar_wait(done, 0u);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  if (p.prof && tid == 0) p.prof[cta * 4 + 1] = globaltimer_ns();
 
   // ---- epilogue: thread = token row m0 + 32*warp + lane (its TMEM lane)
   const int64_t token = m0 + tid;
@@ -410,9 +421,10 @@ __global__ void __launch_bounds__(128, 2)
     // dense_fixup_kernel, which patches the code bit and z_out, so every code
     // is bit-exact.  Rare (|z| < 1e-4); appended to a list here.
     uint32_t fixmask = 0, forced = 0, forced_sign = 0;
+    const float xn = live ? __ldg(p.xnorm + token) * p.fix_scale : 0.f;
 #pragma unroll
     for (int q = 0; q < TAU; ++q)
-      if (fabsf(z[q]) < p.fixup) fixmask |= 1u << q;
+      if (!(fabsf(z[q]) >= xn * __ldg(p.wnorm + c0 + t * TAU + q))) fixmask |= 1u << q;
     if (!live) fixmask = 0;
     if (fixmask) {
       const int cnt = __popc(fixmask);
@@ -465,32 +477,43 @@ __global__ void __launch_bounds__(128, 2)
                  : "memory");
   }
   if (bad) atomicOr(p.flag, bad);
-  if (p.prof && tid == 0) {
-    uint32_t smid;
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    p.prof[cta * 4 + 2] = globaltimer_ns();
-    p.prof[cta * 4 + 3] = smid;
-  }
 }
 
 // Per-call split of x into tf32 hi / lo operands (+ the finiteness check of
 // the projection input, projection.cpp:172).
-__global__ void dense_split_x_kernel(const float* __restrict__ x, int64_t count,
-                                     float* __restrict__ xhi, float* __restrict__ xlo, int* flag,
-                                     int* fix_count) {
+// ||v||_2 of one row by a warp (float64 sum of squares), rounded up so the
+// fixup band stays a bound
+__device__ __forceinline__ float warp_row_norm(double ss) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  return __double2float_ru(sqrt(ss) * (1.0 + 1e-12));
+}
+
+// x -> tf32 hi / lo planes (one warp per row) and ||x_t||_2
+__global__ void dense_split_x_kernel(const float* __restrict__ x, int64_t n, int d_in,
+                                     float* __restrict__ xhi, float* __restrict__ xlo,
+                                     float* __restrict__ xnorm, int* flag, int* fix_count) {
   if (blockIdx.x == 0 && threadIdx.x == 0) *fix_count = 0;  // for the GEMM launched next
+  const int lane = threadIdx.x & 31;
   int bad = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count / 4;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const float4 v = __ldg(reinterpret_cast<const float4*>(x) + i);
-    if (!isfinite(v.x) || !isfinite(v.y) || !isfinite(v.z) || !isfinite(v.w)) bad = 1;
-    float4 h, l;
-    h.x = umma::tf32_rn(v.x); l.x = umma::tf32_rn(v.x - h.x);
-    h.y = umma::tf32_rn(v.y); l.y = umma::tf32_rn(v.y - h.y);
-    h.z = umma::tf32_rn(v.z); l.z = umma::tf32_rn(v.z - h.z);
-    h.w = umma::tf32_rn(v.w); l.w = umma::tf32_rn(v.w - h.w);
-    reinterpret_cast<float4*>(xhi)[i] = h;
-    reinterpret_cast<float4*>(xlo)[i] = l;
+  for (int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < n;
+       row += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    double ss = 0.0;
+    for (int c = lane; c < d_in / 4; c += 32) {
+      const int64_t i = row * (d_in / 4) + c;
+      const float4 v = __ldg(reinterpret_cast<const float4*>(x) + i);
+      if (!isfinite(v.x) || !isfinite(v.y) || !isfinite(v.z) || !isfinite(v.w)) bad = 1;
+      ss += (double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z + (double)v.w * v.w;
+      float4 h, l;
+      h.x = umma::tf32_rn(v.x); l.x = umma::tf32_rn(v.x - h.x);
+      h.y = umma::tf32_rn(v.y); l.y = umma::tf32_rn(v.y - h.y);
+      h.z = umma::tf32_rn(v.z); l.z = umma::tf32_rn(v.z - h.z);
+      h.w = umma::tf32_rn(v.w); l.w = umma::tf32_rn(v.w - h.w);
+      reinterpret_cast<float4*>(xhi)[i] = h;
+      reinterpret_cast<float4*>(xlo)[i] = l;
+    }
+    const float nr = warp_row_norm(ss);
+    if (lane == 0) xnorm[row] = nr;
   }
   if (bad) atomicOr(flag, 1);
 }
@@ -538,25 +561,35 @@ __device__ __forceinline__ void split_bf16x3(float v, __nv_bfloat16& b0, __nv_bf
   b2 = __float2bfloat16_rn(r1 - __bfloat162float(b1));
 }
 
-__global__ void dense_split_x_bf16x3_kernel(const float* __restrict__ x, int64_t count,
+// x -> bf16 x3 planes (one warp per row) and ||x_t||_2
+__global__ void dense_split_x_bf16x3_kernel(const float* __restrict__ x, int64_t n, int d_in,
                                             __nv_bfloat16* __restrict__ x0,
                                             __nv_bfloat16* __restrict__ x1,
-                                            __nv_bfloat16* __restrict__ x2, int* flag,
+                                            __nv_bfloat16* __restrict__ x2,
+                                            float* __restrict__ xnorm, int* flag,
                                             int* fix_count) {
   if (blockIdx.x == 0 && threadIdx.x == 0) *fix_count = 0;  // for the GEMM launched next
+  const int lane = threadIdx.x & 31;
   int bad = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count / 4;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const float4 v = __ldg(reinterpret_cast<const float4*>(x) + i);
-    if (!isfinite(v.x) || !isfinite(v.y) || !isfinite(v.z) || !isfinite(v.w)) bad = 1;
-    __nv_bfloat16 a[4], b[4], c[4];
-    split_bf16x3(v.x, a[0], b[0], c[0]);
-    split_bf16x3(v.y, a[1], b[1], c[1]);
-    split_bf16x3(v.z, a[2], b[2], c[2]);
-    split_bf16x3(v.w, a[3], b[3], c[3]);
-    reinterpret_cast<uint2*>(x0)[i] = *reinterpret_cast<const uint2*>(a);
-    reinterpret_cast<uint2*>(x1)[i] = *reinterpret_cast<const uint2*>(b);
-    reinterpret_cast<uint2*>(x2)[i] = *reinterpret_cast<const uint2*>(c);
+  for (int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < n;
+       row += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    double ss = 0.0;
+    for (int c = lane; c < d_in / 4; c += 32) {
+      const int64_t i = row * (d_in / 4) + c;
+      const float4 v = __ldg(reinterpret_cast<const float4*>(x) + i);
+      if (!isfinite(v.x) || !isfinite(v.y) || !isfinite(v.z) || !isfinite(v.w)) bad = 1;
+      ss += (double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z + (double)v.w * v.w;
+      __nv_bfloat16 a[4], b[4], c3[4];
+      split_bf16x3(v.x, a[0], b[0], c3[0]);
+      split_bf16x3(v.y, a[1], b[1], c3[1]);
+      split_bf16x3(v.z, a[2], b[2], c3[2]);
+      split_bf16x3(v.w, a[3], b[3], c3[3]);
+      reinterpret_cast<uint2*>(x0)[i] = *reinterpret_cast<const uint2*>(a);
+      reinterpret_cast<uint2*>(x1)[i] = *reinterpret_cast<const uint2*>(b);
+      reinterpret_cast<uint2*>(x2)[i] = *reinterpret_cast<const uint2*>(c3);
+    }
+    const float nr = warp_row_norm(ss);
+    if (lane == 0) xnorm[row] = nr;
   }
   if (bad) atomicOr(flag, 1);
 }

@@ -566,120 +566,3 @@ __global__ void __launch_bounds__(256, 2) gather_split_kernel(GatherParams p, in
 }
 
 }  // namespace lffn_gpu
-
-namespace lffn_gpu {
-
-__device__ __forceinline__ void ldgsts16(void* smem_dst, const void* gmem_src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                   static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst))),
-               "l"(gmem_src)
-               : "memory");
-}
-__device__ __forceinline__ void ldgsts_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void ldgsts_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-// Per-warp shared-memory staging of a token's table walk (LDGSTS): lane l
-// copies its own 16-byte pieces of TPS tables' row segments per stage into a
-// ring of NS stages and reads back only what it copied (no cross-lane
-// dependency), so the registers hold just the accumulators.  Used by
-// gather_async_kernel (experiment, LFFN_GATHER_ASYNC) and by the fused kernel.
-template <typename TT, int MAXC, int TPS, int NS>
-struct AsyncWalk {
-  static constexpr int VEC = Raw<TT>::VEC;
-  static constexpr int CHUNK = 32 * VEC;
-  static constexpr int STAGE = TPS * MAXC * 32;  // uint4 per stage
-  static constexpr size_t bytes_per_warp() { return size_t(NS) * STAGE * 16; }
-
-  // acc += sum_k coeff(k) * T_k[code(k)][lane's columns], k = 0 .. nk-1
-  // ascending; code(k) / coeff(k) are read through the callables
-  template <typename CodeAt, typename CoeffAt>
-  static __device__ __forceinline__ void walk(uint4* ring, const TT* T, int64_t tstride, int d_out,
-                                              int nk, int lane, const bool (&ok)[MAXC],
-                                              float (&acc)[MAXC][VEC], CodeAt code_at,
-                                              CoeffAt coeff_at) {
-    const int nst = nk / TPS;
-    const int colbase = lane * VEC;
-    auto issue = [&](int st) {
-      if (st < nst) {
-        uint4* buf = ring + (size_t)(st % NS) * STAGE;
-#pragma unroll
-        for (int q = 0; q < TPS; ++q) {
-          const int k = st * TPS + q;
-          const TT* rp = T + (int64_t)k * tstride + (int64_t)code_at(k) * d_out + colbase;
-#pragma unroll
-          for (int c = 0; c < MAXC; ++c)
-            if (ok[c]) ldgsts16(buf + (q * MAXC + c) * 32 + lane, rp + c * CHUNK);
-        }
-      }
-      ldgsts_commit();
-    };
-#pragma unroll
-    for (int s0 = 0; s0 < NS; ++s0) issue(s0);
-    for (int st = 0; st < nst; ++st) {
-      ldgsts_wait<NS - 1>();
-      const uint4* buf = ring + (size_t)(st % NS) * STAGE;
-      float w[TPS];
-#pragma unroll
-      for (int q = 0; q < TPS; ++q) w[q] = coeff_at(st * TPS + q);
-#pragma unroll
-      for (int q = 0; q < TPS; ++q)
-#pragma unroll
-        for (int c = 0; c < MAXC; ++c) {
-          const uint4 r = ok[c] ? buf[(q * MAXC + c) * 32 + lane] : make_uint4(0u, 0u, 0u, 0u);
-          Raw<TT>::fma(acc[c], w[q], r);
-        }
-      issue(st + NS);
-    }
-    ldgsts_wait<0>();
-  }
-};
-
-// Experimental (LFFN_GATHER_ASYNC="TPS,NS,NW"): the persistent row gather
-// with its in-flight rows in shared memory (AsyncWalk) instead of registers;
-// one warp per token, rec4 layout.  c2 fp32: 0.667 ms vs 0.639 ms for the
-// register kernel, at 88-96 registers instead of 128.
-template <typename TT, int MAXC, int TPS, int NS, int NW>
-__global__ void __launch_bounds__(NW * 32, 1) gather_async_kernel(GatherParams p) {
-  using W = AsyncWalk<TT, MAXC, TPS, NS>;
-  constexpr int VEC = W::VEC;
-  extern __shared__ __align__(16) unsigned char gsm[];
-  const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
-  uint4* ring = reinterpret_cast<uint4*>(gsm) + (size_t)wib * NS * W::STAGE;
-  const int64_t nwarps = (int64_t)gridDim.x * NW;
-  const int nchunks = (p.d_out + W::CHUNK - 1) / W::CHUNK;
-  const TT* T = reinterpret_cast<const TT*>(p.T);
-  const int64_t tstride = (int64_t)p.rows * p.d_out;
-  bool ok[MAXC];
-#pragma unroll
-  for (int c = 0; c < MAXC; ++c) ok[c] = (c < nchunks) && (lane * VEC + c * W::CHUNK < p.d_out);
-  int bad = 0;
-  for (int64_t token = (int64_t)blockIdx.x * NW + wib; token < p.n; token += nwarps) {
-    const uint32_t* cr = p.codes + token * p.ld;
-    const float* wr = p.coeff + token * p.ld;
-    float acc[MAXC][VEC];
-#pragma unroll
-    for (int c = 0; c < MAXC; ++c)
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) acc[c][v] = 0.f;
-    W::walk(ring, T, tstride, p.d_out, p.nk, lane, ok, acc,
-            [&](int k) { return __ldg(cr + k); }, [&](int k) { return __ldg(wr + k); });
-    float* yr = p.y + token * p.d_out;
-#pragma unroll
-    for (int c = 0; c < MAXC; ++c) {
-      if (!ok[c]) continue;
-      const int col = lane * VEC + c * W::CHUNK;
-#pragma unroll
-      for (int v = 0; v < VEC; ++v)
-        if (!isfinite(acc[c][v])) bad = 4;
-#pragma unroll
-      for (int v = 0; v < VEC; v += 4)
-        *reinterpret_cast<float4*>(yr + col + v) =
-            make_float4(acc[c][v], acc[c][v + 1], acc[c][v + 2], acc[c][v + 3]);
-    }
-  }
-  if (bad) atomicOr(p.flag, bad);
-}
-
-}  // namespace lffn_gpu

@@ -17,12 +17,11 @@
 #include <vector>
 
 #include "gather_kernels.cuh"
-#include "fused_kernels.cuh"
 #include "hash_kernels.cuh"
 #include "dense_tcgen05.cuh"
 #include "hash_bh_kernel.cuh"
 #include "backward_kernels.cuh"
-#include "hash_pair_kernel.cuh"
+#include "hash_sf_kernel.cuh"
 #include "lffn_gpu.h"
 #include "lffn_internal.h"
 #include "neighbor_kernels.cuh"
@@ -87,12 +86,12 @@ struct lffn_ctx {
   int dense_exact = 0;       // 1: exact float64 dense projection
   alignas(64) DenseMaps dense_maps{};  // TMA maps of the split planes (dense)
   void* d_xp[3] = {nullptr, nullptr, nullptr};  // dense: per-call split of x (max_tokens x d_in)
-  int dense_split = kSplitTf32;  // kSplitTf32 | kSplitBf16x3 (LFFN_DENSE_SPLIT=bf16x3)
+  int dense_split = kSplitTf32;  // kSplitTf32 | kSplitBf16x3 (bf16 x3 when d_in % 8 == 0)
   uint2* d_fix_list = nullptr;  // dense tcgen05: deferred exact fixups
+  float* d_xnorm = nullptr;     // dense tcgen05: ||x_t||_2 per token (fixup band)
+  float* d_wnorm = nullptr;     // dense tcgen05: ||W[:, c]||_2 per slice column
   int* d_fix_count = nullptr;
   int fix_cap = 0;
-  long long* d_dense_prof = nullptr;  // LFFN_DENSE_PROF: per-CTA timestamps (debug)
-  int64_t dense_prof_len = 0;
   double* d_zbuf = nullptr;  // dense: [max_tokens x code_width] float64
   // backward scratch (allocated by the first lffn_backward / lffn_proj_backward)
   double* d_gzbuf = nullptr;       // [max_tokens x code_width] float64 grad_z
@@ -127,8 +126,11 @@ struct lffn_ctx {
   int num_sms = 148;
   size_t table_group_bytes = 0;  // >0: walk tables in groups of this many bytes (measured slower on c2)
   int64_t gather_variant = 0;    // LFFN_OPT_GATHER_VARIANT (0 = default choice)
-  int fused = 0;                 // LFFN_OPT_FUSED: 1 = one-kernel hash + gather (opt-in)
   int bf16w = 1;                 // LFFN_OPT_BF16_COEFF_FMA: exact FHFMA path for bf16 tables
+  int bwd_one_pass = 0;          // LFFN_OPT_BWD_ONE_PASS: single-pass KB1 (A/B reference)
+  int hash_exact = 0;            // LFFN_OPT_HASH_EXACT: always K1 (z bit-identical)
+  int host_chunks = 8;           // LFFN_OPT_HOST_CHUNKS: lffn_forward_host pipeline chunks
+  unsigned long long* d_sfmask = nullptr;  // K1f: per-thread sign masks [3][D/64]
 };
 
 namespace {
@@ -140,7 +142,6 @@ int flag_message(int flag) {
   if (flag & kFlagBwdInput) return fail(LFFN_ERR_NUMERIC, "non-finite values in lookup backward input");
   if (flag & kFlagBwdOutput) return fail(LFFN_ERR_NUMERIC, "non-finite values in projection backward output");
   if (flag & kFlagBwdTables) return fail(LFFN_ERR_NUMERIC, "non-finite values in lookup backward tables");
-  if (flag & kFlagStream) return fail(LFFN_ERR_RUNTIME, "device-side wait timed out (fused kernel ring)");
   return LFFN_OK;
 }
 
@@ -177,17 +178,10 @@ void destroy_ctx(lffn_ctx* c) {
   cudaFree(c->d_wt64);
   for (int q = 0; q < 3; ++q) cudaFree(c->d_xp[q]);
   cudaFree(c->d_fix_list);
+  cudaFree(c->d_xnorm);
+  cudaFree(c->d_wnorm);
   cudaFree(c->d_fix_count);
-  if (c->d_dense_prof) {
-    // debug dump: [cta][start, mainloop done, end, smid] globaltimer ns
-    std::vector<long long> h(size_t(c->dense_prof_len));
-    cudaMemcpy(h.data(), c->d_dense_prof, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
-    if (FILE* f = fopen(getenv("LFFN_DENSE_PROF"), "wb")) {
-      fwrite(h.data(), sizeof(long long), h.size(), f);
-      fclose(f);
-    }
-    cudaFree(c->d_dense_prof);
-  }
+  cudaFree(c->d_sfmask);
   cudaFree(c->d_zbuf);
   cudaFree(c->d_gzbuf);
   cudaFree(c->d_bwd_offs);
@@ -423,34 +417,27 @@ int launch_hash_top1(lffn_ctx* c, const float* d_x, int64_t n, uint32_t* codes, 
     d.codes = codes;
     d.coeff = coeff;
     d.flag = c->d_flag;
-    static const float fix = getenv("LFFN_DENSE_FIXUP") ? float(atof(getenv("LFFN_DENSE_FIXUP"))) : kDenseFixup;
-    d.fixup = fix;
+    d.fix_scale = dense_fix_scale(d.d_in);
+    d.xnorm = c->d_xnorm;
+    d.wnorm = c->d_wnorm;
     d.fix_list = c->d_fix_list;
     d.fix_count = c->d_fix_count;
     d.fix_cap = c->fix_cap;
     // split x into tf32 hi / lo (ctx scratch; the TMA maps are built once)
-    const int64_t cnt = n * c->cfg.d_in;
-    const unsigned gs = unsigned(std::min<int64_t>(int64_t(c->num_sms) * 8, (cnt / 4 + 255) / 256 + 1));
+    const unsigned gs = unsigned(std::min<int64_t>(int64_t(c->num_sms) * 8, (n * 32 + 255) / 256));
+    const int din = int(c->cfg.d_in);
     if (c->dense_split != kSplitTf32)
       dense_split_x_bf16x3_kernel<<<gs, 256, 0, st>>>(
-          d_x, cnt, static_cast<__nv_bfloat16*>(c->d_xp[0]), static_cast<__nv_bfloat16*>(c->d_xp[1]),
-          static_cast<__nv_bfloat16*>(c->d_xp[2]), c->d_flag, c->d_fix_count);
+          d_x, n, din, static_cast<__nv_bfloat16*>(c->d_xp[0]), static_cast<__nv_bfloat16*>(c->d_xp[1]),
+          static_cast<__nv_bfloat16*>(c->d_xp[2]), c->d_xnorm, c->d_flag, c->d_fix_count);
     else
-      dense_split_x_kernel<<<gs, 256, 0, st>>>(d_x, cnt, static_cast<float*>(c->d_xp[0]),
-                                               static_cast<float*>(c->d_xp[1]), c->d_flag, c->d_fix_count);
+      dense_split_x_kernel<<<gs, 256, 0, st>>>(d_x, n, din, static_cast<float*>(c->d_xp[0]),
+                                               static_cast<float*>(c->d_xp[1]), c->d_xnorm, c->d_flag,
+                                               c->d_fix_count);
     ++c->launches;
     const size_t smem = dense_smem_bytes(d.ntile, c->dense_split);
 
     dim3 grid((unsigned)((d.ncols + d.ntile - 1) / d.ntile), (unsigned)((n + umma::BM - 1) / umma::BM));
-    if (getenv("LFFN_DENSE_PROF")) {
-      const int64_t len = int64_t(grid.x) * grid.y * 4;
-      if (len > c->dense_prof_len) {
-        cudaFree(c->d_dense_prof);
-        cudaMalloc(&c->d_dense_prof, size_t(len) * sizeof(long long));
-        c->dense_prof_len = len;
-      }
-      d.prof = c->d_dense_prof;
-    }
     const int rc = launch_dense_tcgen05(int(c->cfg.code_bits), c->dense_split, grid, smem, st,
                                         c->dense_maps, d);
     if (rc != LFFN_OK) return rc;
@@ -475,65 +462,65 @@ int launch_hash_top1(lffn_ctx* c, const float* d_x, int64_t n, uint32_t* codes, 
     ++c->launches;
     p.z_in = c->d_zbuf;
   }
+  const int kind = c->proj.kind == LFFN_PROJ_SIGNFLIP ? kPreSign
+                   : c->proj.kind == LFFN_PROJ_ACDC   ? kPreDiag
+                                                      : kPreNone;
+  if (kind == kPreSign && c->d_sfmask && !z_out && !exact_z && !c->hash_exact && !p.scaled &&
+      n > 16) {
+    // K1f (hash_sf_kernel.cuh): the production signflip hash at D = 2048 /
+    // 4096 -- three transposes per token, codes from warp ballots; z not
+    // bit-identical (stage order), codes bit-exact wherever |z| > 1e-5
+    HashSfParams q{};
+    q.x = d_x;
+    q.n = n;
+    q.d_in = int(c->cfg.d_in);
+    q.code_width = int(c->code_width);
+    q.tau = int(c->cfg.code_bits);
+    q.kb = int(c->kb);
+    q.ke = int(c->ke);
+    q.masks = c->d_sfmask;
+    q.codes = codes;
+    q.coeff = coeff;
+    q.flag = c->d_flag;
+    auto gof = [&](auto kernel, int logd) {
+      const int tpt = (1 << logd) / 64, tpb = 128 / tpt;
+      const int slot = (1 << logd) + 2 * ((1 << logd) >> 6) + (1 << logd) / 32;
+      const size_t smem = size_t(tpb) * size_t(slot) * sizeof(double);
+      set_smem(reinterpret_cast<const void*>(kernel), int(smem));
+      kernel<<<unsigned((n + tpb - 1) / tpb), 128, smem, st>>>(q);
+    };
+    if (c->logD == 11) gof(hash_sf_kernel<11>, 11);
+    else gof(hash_sf_kernel<12>, 12);
+    ++c->launches;
+    LFFN_CUDA(cudaGetLastError());
+    return LFFN_OK;
+  }
   int loge = c->logD >= kMaxLogE ? kMaxLogE : int(c->logD);
   // a handful of tokens cannot fill the GPU: 16 coordinates per thread (4x
   // the threads per token) shortens each token's serial chain (c5, n = 1:
   // 14.9 -> 12.9 us)
   if (n <= 16 && loge == 6 && (c->D >> 4) <= 256) loge = 4;
-  if (const char* ov = getenv("LFFN_HASH_LOGE")) {  // tuning override
-    const int o = atoi(ov);
-    if (o >= 1 && o < loge && (c->D >> o) <= 256) loge = o;
-  }
   const int E = 1 << loge;
   const int tpt = int(c->D / E);  // <= 256 for D <= 16384
-  // LOGE 6 (one warp per D <= 2048 token, ~214 registers): 128-thread CTAs
-  // measured fastest (c2 hash 0.233 ms vs 0.251 ms with 256-thread CTAs)
-  static const int hvar = getenv("LFFN_HASH_VARIANT") ? atoi(getenv("LFFN_HASH_VARIANT")) : 2;
-  const int nt = (hvar > 0 && loge == 6 && tpt <= 128) ? 128 : 256;
+  // LOGE 6 (one warp per D <= 2048 token): 128-thread CTAs measured fastest
+  // (c2 hash 0.233 ms vs 0.251 ms with 256-thread CTAs)
+  const int nt = (loge == 6 && tpt <= 128) ? 128 : 256;
   const int block = std::max(tpt, (nt / tpt) * tpt);
   const int tpb = block / tpt;
   p.tokens_per_block = tpb;
   p.threads_per_token = tpt;
   const size_t smem = size_t(tpb) * size_t(padded_len(int(c->D))) * sizeof(double);
   const unsigned grid = (unsigned)((n + tpb - 1) / tpb);
-  const int kind = c->proj.kind == LFFN_PROJ_SIGNFLIP ? kPreSign
-                   : c->proj.kind == LFFN_PROJ_ACDC   ? kPreDiag
-                                                      : kPreNone;
   auto go = [&](auto kernel) {
     set_smem(reinterpret_cast<const void*>(kernel), int(smem));
     kernel<<<grid, block, smem, st>>>(p);
   };
-  // the pair kernel is exact but measured slower (shuffle traffic throttles
-  // the MIO queue: c2 hash 0.46 vs 0.23 ms), so it is opt-in
-  static const int use_pair = getenv("LFFN_HASH_PAIR") ? atoi(getenv("LFFN_HASH_PAIR")) : 0;
-  if (use_pair && (c->logD == 11 || c->logD == 12) && kind != kPreNone) {
-    // D = 2048 / 4096: the 32-element pair kernel (hash_pair_kernel.cuh)
-    const int tpb2 = c->logD == 11 ? 2 : 1;
-    const size_t smem2 = size_t(tpb2) * size_t(pair_padded_len(int(c->D))) * sizeof(double);
-    const unsigned grid2 = (unsigned)((n + tpb2 - 1) / tpb2);
-    auto go2 = [&](auto kernel) {
-      set_smem(reinterpret_cast<const void*>(kernel), int(smem2));
-      kernel<<<grid2, 128, smem2, st>>>(p);
-    };
-    if (c->logD == 11) {
-      if (kind == kPreSign) go2(hash_pair_kernel<11, kPreSign>);
-      else go2(hash_pair_kernel<11, kPreDiag>);
-    } else {
-      if (kind == kPreSign) go2(hash_pair_kernel<12, kPreSign>);
-      else go2(hash_pair_kernel<12, kPreDiag>);
-    }
-    ++c->launches;
-    LFFN_CUDA(cudaGetLastError());
-    return LFFN_OK;
-  }
-  if (nt == 128 && kind == kPreSign) {  // tuning variants (LFFN_HASH_VARIANT)
+  if (nt == 128 && kind == kPreSign) {
     // compile-time geometry for the BASELINE widths (D = 2048: c2, c3, c5;
     // D = 4096: c4) and the signflip transform count
     if (c->logD == 11 && c->n_transforms == 3) go(hash_structured_kernel<6, kPreSign, 128, 3, 11, 3>);
     else if (c->logD == 12 && c->n_transforms == 3) go(hash_structured_kernel<6, kPreSign, 128, 3, 12, 3>);
-    else if (hvar == 1) go(hash_structured_kernel<6, kPreSign, 128, 3>);
-    else if (hvar == 2) go(hash_structured_kernel<6, kPreSign, 128, 2>);
-    else go(hash_structured_kernel<6, kPreSign, 128, 4>);
+    else go(hash_structured_kernel<6, kPreSign, 128, 2>);
     ++c->launches;
     LFFN_CUDA(cudaGetLastError());
     return LFFN_OK;
@@ -589,8 +576,7 @@ int launch_gather_group(lffn_ctx* c, const uint32_t* codes, const float* coeff, 
   // coefficient FMA, measured +4% (c2 bf16) and +4% (c3) for bf16 tables
   // walked one warp per token, -6% for c4 (four warps per token,
   // part-major) and -2% for c2 fp32; set per launch below
-  static const int rev = getenv("LFFN_GATHER_REVERSE") ? atoi(getenv("LFFN_GATHER_REVERSE")) : -1;
-  p.reverse_odd_rounds = rev >= 0 ? rev : (c->t_dtype == LFFN_BF16 ? 1 : 0);
+  p.reverse_odd_rounds = c->t_dtype == LFFN_BF16 ? 1 : 0;
   const bool f32 = c->t_dtype == LFFN_F32;
   const int vec = f32 ? ((p.d_out % 4 == 0) ? 4 : 1) : ((p.d_out % 8 == 0) ? 8 : 1);
   if (vec > 1 && p.nc == 1) {
@@ -604,47 +590,16 @@ int launch_gather_group(lffn_ctx* c, const uint32_t* codes, const float* coeff, 
                       (reinterpret_cast<uintptr_t>(p.coeff) % 16 == 0);
     const int64_t warps = n * wpt;
     const unsigned grid = (unsigned)((warps * 32 + 255) / 256);
-    static const char* gasync = getenv("LFFN_GATHER_ASYNC");  // experiment: "TPS,NS,NW"
-    if (gasync && rec4 && !p.accumulate) {
-      int tps = 2, ns = 2, nw = 16;
-      sscanf(gasync, "%d,%d,%d", &tps, &ns, &nw);
-      using AF = void (*)(GatherParams);
-      AF fn = nullptr;
-      int mc = 0;
-#define LFFN_GA(TT, M, TP, NSV, NWV) \
-  if (tps == TP && ns == NSV && nw == NWV) fn = &gather_async_kernel<TT, M, TP, NSV, NWV>, mc = M;
-      if (f32 && nchunks == 6) {
-        LFFN_GA(float, 6, 2, 2, 16) LFFN_GA(float, 6, 1, 3, 16)
-      }
-#undef LFFN_GA
-      if (fn && (p.nk % tps) == 0 && nchunks <= mc) {
-        const size_t smem = size_t(nw) * ns * tps * mc * 32 * 16;
-        set_smem(reinterpret_cast<const void*>(fn), int(smem));
-        const unsigned g = unsigned(std::min<int64_t>(c->num_sms, (n + nw - 1) / nw));
-        fn<<<g, nw * 32, smem, st>>>(p);
-        ++c->launches;
-        LFFN_CUDA(cudaGetLastError());
-        return LFFN_OK;
-      }
-    }
     if (rec4) {
       // persistent row kernel: grid = 2 CTAs per SM; 4 tables' packed rows
       // in flight per lane (the f32 6-chunk case keeps 4 x 6 x 16 B)
       const unsigned pg = (unsigned)std::min<int64_t>(int64_t(c->num_sms) * 2, (warps * 32 + 255) / 256);
       // (MAXC 2 for bf16 -- 2x the column parts, half the bytes in flight per
       // warp -- measured slower: c3 1.39 vs 1.22 ms, c4 2.47 vs 2.07 ms)
-      int pmaxc = f32 ? maxc : (nchunks <= 2 ? 2 : nchunks <= 3 ? 3 : 4);
-      int ptif = 4;
-      static const char* bcfg = getenv("LFFN_GATHER_BF16_CFG");  // tuning: "MAXC,TIF"
-      if (!f32 && bcfg) {
-        int m = 0, t = 0;
-        if (sscanf(bcfg, "%d,%d", &m, &t) == 2 && ((m == 2 && t == 8) || (m == 1 && t == 8) ||
-                                                   (m == 4 && t == 2) || (m == 2 && t == 4)))
-          pmaxc = m, ptif = t;
-      }
+      const int pmaxc = f32 ? maxc : (nchunks <= 2 ? 2 : nchunks <= 3 ? 3 : 4);
       const int pwpt = (nchunks + pmaxc - 1) / pmaxc;
       const int64_t pwarps = n * pwpt;
-      if (rev < 0 && pwpt > 1) p.reverse_odd_rounds = 0;
+      if (pwpt > 1) p.reverse_odd_rounds = 0;
       const unsigned pgrid = (unsigned)std::min<int64_t>(int64_t(c->num_sms) * 2, (pwarps * 32 + 255) / 256);
       (void)pg;
       // fewer (token, part) items than resident warp slots: split the table
@@ -674,6 +629,23 @@ int launch_gather_group(lffn_ctx* c, const uint32_t* codes, const float* coeff, 
         LFFN_CUDA(cudaGetLastError());
         return LFFN_OK;
       }
+      // Narrow part-major walk (gather_variant 1): one 256-column (bf16) /
+      // 128-column (fp32) chunk per warp, 8 tables in flight per lane, 4
+      // (bf16: 3) CTAs per SM, items part-major, so a round of resident warps touches
+      // 1/nchunks of every row -- the working set of a table stack larger
+      // than L2 (c3: 268 MB -> 67 MB per part) stays L2-resident.
+      const bool narrow = c->gather_variant == 1 && nchunks >= 2 && p.nk % 8 == 0 && S == 1;
+      if (narrow) {
+        const int64_t nwarps_n = n * nchunks;
+        const int minb = f32 ? 4 : 3;  // bf16: 85 registers (64 spill)
+        const unsigned ngrid = (unsigned)std::min<int64_t>(int64_t(c->num_sms) * minb, (nwarps_n * 32 + 255) / 256);
+        p.reverse_odd_rounds = 0;
+        if (f32) gather_row_persistent_kernel<float, 1, 8, 4, true><<<ngrid, 256, 0, st>>>(p, nchunks);
+        else gather_row_persistent_kernel<__nv_bfloat16, 1, 8, 3, true><<<ngrid, 256, 0, st>>>(p, nchunks);
+        ++c->launches;
+        LFFN_CUDA(cudaGetLastError());
+        return LFFN_OK;
+      }
       // (measured at c2 fp32: one warp per token with 6 chunks and 2 CTAs/SM
       // beats 2-3 warps per token at 3-4 CTAs/SM, 0.641 vs 0.698-0.942 ms;
       // L2 evict_last/evict_first splits of the table stack: 0.68-0.81 ms)
@@ -690,10 +662,7 @@ int launch_gather_group(lffn_ctx* c, const uint32_t* codes, const float* coeff, 
         if (pmaxc == 2) { LFFN_PROW(float, 2, 4) } else if (pmaxc == 4) { LFFN_PROW(float, 4, 4) }
         else { LFFN_PROW(float, 6, 4) }
       } else {
-        if (pmaxc == 2 && ptif == 8) { LFFN_PROW(__nv_bfloat16, 2, 8) }
-        else if (pmaxc == 1) { LFFN_PROW(__nv_bfloat16, 1, 8) }
-        else if (pmaxc == 4 && ptif == 2) { LFFN_PROW(__nv_bfloat16, 4, 2) }
-        else if (pmaxc == 2) { LFFN_PROW(__nv_bfloat16, 2, 4) } else if (pmaxc == 3) { LFFN_PROW(__nv_bfloat16, 3, 4) } else { LFFN_PROW(__nv_bfloat16, 4, 4) }
+        if (pmaxc == 2) { LFFN_PROW(__nv_bfloat16, 2, 4) } else if (pmaxc == 3) { LFFN_PROW(__nv_bfloat16, 3, 4) } else { LFFN_PROW(__nv_bfloat16, 4, 4) }
       }
 #undef LFFN_PROW
       ++c->launches;
@@ -758,115 +727,9 @@ int launch_gather(lffn_ctx* c, const uint32_t* codes, const float* coeff, int64_
   return LFFN_OK;
 }
 
-// K13: hash + gather in one persistent kernel (fused_kernels.cuh) for the
-// signflip projection at D = 2048 with tau 8 / 10 (BASELINE c2, c3, c5).
-// Returns 1 (nothing launched) when the shape is not covered.
-using FusedFn = void (*)(FusedParams);
-struct FusedChoice {
-  FusedFn fn = nullptr;
-  int maxc = 0, block = 128;
-  int hp = 0, ring = 0;  // warp-specialised kernel: hash pairs, ring slots (0 = same-warp kernel)
-  int gw = 0, ans = 0;   // gather warps; shared-memory row stages per gather warp (0 = registers)
-};
-
-// LFFN_OPT_FUSED 1: warp-specialised fused_ws_kernel (opt-in: measured
-// slower than the two kernels, fused_kernels.cuh)
-FusedChoice fused_choice(const lffn_ctx* c) {
-  FusedChoice f;
-  if (!c->fused || c->nc != 1 || c->proj.kind != LFFN_PROJ_SIGNFLIP || c->n_transforms != 3 ||
-      c->logD != 11 || c->h_loc == 0 || c->h_loc % 4 != 0)
-    return f;
-  const int tau = int(c->cfg.code_bits);
-  const int64_t d_out = c->cfg.d_out;
-  const bool f32 = c->t_dtype == LFFN_F32;
-  if (d_out % (f32 ? 4 : 8) != 0) return f;
-  const int64_t nchunks = (d_out + (f32 ? 128 : 256) - 1) / (f32 ? 128 : 256);
-  static const int hp = getenv("LFFN_FUSED_HP") ? atoi(getenv("LFFN_FUSED_HP")) : 2;
-  // LFFN_FUSED_ASYNC="GW,NS": gather warps with shared-memory row stages
-  static const char* fa = getenv("LFFN_FUSED_ASYNC");
-  if (fa && f32 && tau == 8 && nchunks == 6) {
-    int gw = 16, ns = 3;
-    sscanf(fa, "%d,%d", &gw, &ns);
-    if (gw == 16 && ns == 3) f = FusedChoice{&fused_ws_kernel<float, 8, 6, 2, 16, 16, 3>, 6, 32 * 20, 2, 16, 16, 3};
-    if (f.fn) return f;
-  }
-  constexpr int R = 32;
-#define LFFN_WS(TT, TAU, M)                                                          \
-  (hp == 3 ? FusedChoice{&fused_ws_kernel<TT, TAU, M, 3, R>, M, 512, 3, R}           \
-             : FusedChoice{&fused_ws_kernel<TT, TAU, M, 2, R>, M, 512, 2, R})
-  if (f32 && tau == 8 && nchunks == 6) f = LFFN_WS(float, 8, 6);
-  else if (!f32 && tau == 8 && nchunks == 3) f = LFFN_WS(__nv_bfloat16, 8, 3);
-  else if (!f32 && tau == 10 && nchunks == 4) f = LFFN_WS(__nv_bfloat16, 10, 4);
-#undef LFFN_WS
-  if (int64_t(c->h_loc) * 8 * f.ring > 160 * 1024) f = FusedChoice{};  // ring must fit
-  return f;
-}
-
-// fills the hash / gather halves of FusedParams as the two-kernel path would
-void fill_hash_params(const lffn_ctx* c, HashParams& p, const float* d_x, int64_t n);
-
-int launch_fused(lffn_ctx* c, const FusedChoice& f, const float* d_x, int64_t n, float* d_y,
-                 const int* ready, int* done, int64_t chunk_tokens, cudaStream_t st) {
-  FusedParams fp{};
-  fill_hash_params(c, fp.h, d_x, n);
-  GatherParams& g = fp.g;
-  g.T = c->d_T;
-  g.y = d_y;
-  g.n = n;
-  g.ld = int(c->h_loc);
-  g.nk = int(c->h_loc);
-  g.nc = 1;
-  g.rows = int(c->rows);
-  g.d_out = int(c->cfg.d_out);
-  g.flag = c->d_flag;
-  const int chunk = c->t_dtype == LFFN_F32 ? 128 : 256;
-  const int nchunks = int((c->cfg.d_out + chunk - 1) / chunk);
-  fp.parts = (nchunks + f.maxc - 1) / f.maxc;
-  fp.ready = ready;
-  fp.done = done;
-  fp.chunk_tokens = chunk_tokens > 0 ? chunk_tokens : n;
-  fp.spin_limit = int64_t(1) << 24;  // ~4 s of 256 ns sleeps
-  static const int dbg = getenv("LFFN_FUSED_DEBUG") ? atoi(getenv("LFFN_FUSED_DEBUG")) : 0;
-  fp.debug_mode = dbg;
-  size_t smem;
-  unsigned grid;
-  if (f.hp > 0) {
-    // one 16-warp CTA per SM, each owning a contiguous token range
-    const size_t slot = size_t((c->h_loc * 8 + 15) / 16 * 16);
-    smem = size_t(16) * f.ring + size_t(f.hp) * size_t(padded_len(int(c->D))) * sizeof(double) +
-           size_t(f.ring) * slot;
-    if (f.ans > 0) smem += size_t(f.gw) * f.ans * f.maxc * 32 * 16;
-    grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(int64_t(c->num_sms), (n + 15) / 16)));
-  } else {
-    return fail(LFFN_ERR_USAGE, "fused forward: no kernel for this shape");
-  }
-  set_smem(reinterpret_cast<const void*>(f.fn), int(smem));
-  f.fn<<<grid, f.block, smem, st>>>(fp);
-  ++c->launches;
-  LFFN_CUDA(cudaGetLastError());
-  return LFFN_OK;
-}
-
-// the fused kernel runs one warp per token: below ~2 rounds of resident
-// warps the split gather (several warps per token) finishes first
-bool use_fused(const lffn_ctx* c, int64_t n) {
-  static const int64_t min_n = getenv("LFFN_FUSED_MIN_TOKENS") ? atol(getenv("LFFN_FUSED_MIN_TOKENS")) : 4096;
-  return n >= min_n && fused_choice(c).fn != nullptr && c->d_T != nullptr;
-}
-
 int forward_impl(lffn_ctx* c, const float* d_x, int64_t n, float* d_y, cudaStream_t st) {
   const bool tm = c->timing;
   if (tm) LFFN_CUDA(cudaEventRecord(c->ev_t0, st));
-  if (use_fused(c, n)) {
-    // one kernel: the whole forward is reported as the gather stage
-    if (tm) LFFN_CUDA(cudaEventRecord(c->ev_t1, st));
-    if (int rc = launch_fused(c, fused_choice(c), d_x, n, d_y, nullptr, nullptr, 0, st)) return rc;
-    if (tm) {
-      LFFN_CUDA(cudaEventRecord(c->ev_t2, st));
-      c->timed = true;
-    }
-    return LFFN_OK;
-  }
   if (int rc = launch_hash(c, d_x, n, c->d_codes, c->d_coeff, nullptr, st)) return rc;
   if (tm) LFFN_CUDA(cudaEventRecord(c->ev_t1, st));
   if (int rc = launch_gather(c, c->d_codes, c->d_coeff, n, d_y, 0, st)) return rc;
@@ -1043,6 +906,21 @@ int lffn_ctx_create_shard(lffn_ctx** out, int device, int64_t max_tokens, const 
       }
     CK(cudaMalloc(&c->d_signmask, mask.size() * sizeof(uint32_t)));
     CK(cudaMemcpy(c->d_signmask, mask.data(), mask.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    if (D == 2048 || D == 4096) {
+      // K1f sign masks in its register layouts (hash_sf_kernel.cuh): thread
+      // t, register r holds index 64 t + r (layout A: transforms 0 and 2) or
+      // t + (D / 64) r (layout B: transform 1)
+      const int64_t tpt = D / 64;
+      std::vector<unsigned long long> sf(size_t(3 * tpt), 0ull);
+      for (int64_t tr = 0; tr < 3; ++tr)
+        for (int64_t t = 0; t < tpt; ++t)
+          for (int64_t r = 0; r < 64; ++r) {
+            const int64_t j = tr == 1 ? t + tpt * r : 64 * t + r;
+            if (blob[tr * D + j] == -1.0) sf[size_t(tr * tpt + t)] |= 1ull << r;
+          }
+      CK(cudaMalloc(&c->d_sfmask, sf.size() * sizeof(unsigned long long)));
+      CK(cudaMemcpy(c->d_sfmask, sf.data(), sf.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+    }
   } else if (proj->kind == LFFN_PROJ_ACDC) {
     c->n_transforms = int(2 * proj->depth);
     CK(cudaMalloc(&c->d_diag, size_t(2 * proj->depth * D) * sizeof(double)));
@@ -1069,8 +947,6 @@ int lffn_ctx_create_shard(lffn_ctx** out, int device, int64_t max_tokens, const 
       // 25% fewer operand bytes, c2 dense hash 0.312 vs 0.336 ms), else tf32
       // hi / lo (LFFN_DENSE_SPLIT=tf32 forces it)
       c->dense_split = proj->d_in % 8 == 0 ? kSplitBf16x3 : kSplitTf32;
-      if (const char* e = getenv("LFFN_DENSE_SPLIT"))
-        if (std::string(e) == "tf32") c->dense_split = kSplitTf32;
       const bool bf = c->dense_split != kSplitTf32;
       const int P = bf ? 3 : 2;
       const size_t eb = bf ? 2 : 4;
@@ -1096,10 +972,25 @@ int lffn_ctx_create_shard(lffn_ctx** out, int device, int64_t max_tokens, const 
       if (c->dense_ntile > 0) {
         const size_t nx = size_t(std::max<int64_t>(max_tokens, 1)) * size_t(proj->d_in);
         for (int q = 0; q < P; ++q) CK(cudaMalloc(&c->d_xp[q], nx * eb));
-        // |z| < 1e-4 is ~1e-4 of the z for Gaussian-like projections; 1M
-        // entries (8 MB) covers 4096 x 2048 all-candidate tiles before the
-        // kernel falls back to inline recomputation
-        c->fix_cap = 1 << 20;
+        // the fixup band holds ~1e-3 of the z for Gaussian-like projections
+        // (c2: ~1.5 per token); 4M entries (32 MB) before the kernel falls
+        // back to inline recomputation
+        c->fix_cap = 1 << 22;
+        CK(cudaMalloc(&c->d_xnorm, nx / size_t(proj->d_in) * sizeof(float)));
+        {
+          std::vector<float> wn(static_cast<size_t>(ncols));
+          for (int64_t col = 0; col < ncols; ++col) {
+            double ss = 0.0;
+            for (int64_t k = 0; k < proj->d_in; ++k) {
+              const double wv = blob[size_t(k * c->code_width + c->kb * cfg->code_bits + col)];
+              ss += wv * wv;
+            }
+            wn[size_t(col)] = float(std::sqrt(ss) * (1.0 + 1e-12));
+            if (double(wn[size_t(col)]) < std::sqrt(ss)) wn[size_t(col)] = std::nextafter(wn[size_t(col)], 1e30f);
+          }
+          CK(cudaMalloc(&c->d_wnorm, wn.size() * sizeof(float)));
+          CK(cudaMemcpy(c->d_wnorm, wn.data(), wn.size() * sizeof(float), cudaMemcpyHostToDevice));
+        }
         CK(cudaMalloc(&c->d_fix_list, size_t(c->fix_cap) * sizeof(uint2)));
         CK(cudaMalloc(&c->d_fix_count, sizeof(int)));
         CK(cudaMemset(c->d_fix_count, 0, sizeof(int)));
@@ -1109,7 +1000,6 @@ int lffn_ctx_create_shard(lffn_ctx** out, int device, int64_t max_tokens, const 
             c->dense_ntile = 0;
       }
     }
-    if (const char* e = getenv("LFFN_DENSE_EXACT")) c->dense_exact = atoi(e);
   }
 
   const size_t mt = size_t(std::max<int64_t>(max_tokens, 1));
@@ -1132,7 +1022,6 @@ int lffn_ctx_create_shard(lffn_ctx** out, int device, int64_t max_tokens, const 
   CK(cudaEventCreate(&c->ev_t1));
   CK(cudaEventCreate(&c->ev_t2));
   c->num_sms = prop.multiProcessorCount;
-  if (const char* g = getenv("LFFN_TABLE_GROUP_MB")) c->table_group_bytes = size_t(atol(g)) << 20;
 #undef CK
   *out = c;
   return LFFN_OK;
@@ -1262,8 +1151,7 @@ int lffn_forward_host(lffn_ctx* c, const float* h_x, int64_t n, float* h_y) {
   // chunk alone does not fill the GPU); the dense kind keeps one stream (its
   // split-x / fixup scratch is per context).
   const int64_t d_in = c->cfg.d_in, d_out = c->cfg.d_out;
-  static const int want = getenv("LFFN_HOST_CHUNKS") ? atoi(getenv("LFFN_HOST_CHUNKS")) : 8;
-  int nch = int(std::min<int64_t>(std::min(want, lffn_ctx::kChunks), std::max<int64_t>(1, n / 512)));
+  int nch = int(std::min<int64_t>(std::min(c->host_chunks, lffn_ctx::kChunks), std::max<int64_t>(1, n / 512)));
   const bool dual = c->proj.kind != LFFN_PROJ_DENSE && c->nc == 1;
   const int64_t per = (n + nch - 1) / nch;
   for (int i = 0; i < nch; ++i) {
@@ -1463,9 +1351,8 @@ int launch_proj_backward(lffn_ctx* c, const float* d_x, const double* gz, int64_
       // grad_W = x^T g: its K (tokens) must stay sequential, so the output
       // tiles are all the parallelism -- 32 x 32 tiles when 64 x 64 ones
       // would not fill the SMs a few times over
-      static const int gw4 = getenv("LFFN_GRADW_TILE32") ? atoi(getenv("LFFN_GRADW_TILE32")) : 1;
       const int64_t tiles64 = int64_t((cw + 63) / 64) * ((d_in + 63) / 64);
-      if (gw4 && tiles64 < int64_t(c->num_sms) * 8) {
+      if (tiles64 < int64_t(c->num_sms) * 8) {
         dim3 grid(unsigned((cw + 31) / 32), unsigned((d_in + 31) / 32));
         gemm_f64_exact4_kernel<float, true, false><<<grid, 64, 0, st>>>(d_x, d_in, gz, cw, d_grad_proj, cw,
                                                                        d_in, cw, int(n), c->d_flag);
@@ -1594,8 +1481,7 @@ int lffn_backward(lffn_ctx* c, const float* d_x, const float* d_grad_y, int64_t 
       // loads); otherwise 4 (fp32 16-byte / bf16 8-byte loads)
       const bool v8 = esz == 2 && c->cfg.d_out % 8 == 0;
       const int mc = int((c->cfg.d_out + (v8 ? 255 : 127)) / (v8 ? 256 : 128));  // chunks per lane
-      static const int one_pass = getenv("LFFN_BWD_ONE_PASS") ? atoi(getenv("LFFN_BWD_ONE_PASS")) : 0;
-      if (v4 && mc <= (v8 ? 4 : 8) && c->cfg.code_bits <= 24 && !one_pass) {
+      if (v4 && mc <= (v8 ? 4 : 8) && c->cfg.code_bits <= 24 && !c->bwd_one_pass) {
         // KB1a gdot per record (many rows in flight), KB1b gz per (token, table)
         const unsigned gg = unsigned(std::min<int64_t>(int64_t(c->num_sms) * 2, (n * 32 + 255) / 256));
 #define LFFN_GDOT(TT, M, V) \
@@ -1675,13 +1561,20 @@ int lffn_ctx_set_option(lffn_ctx* c, int option, int64_t value) {
       c->dense_exact = value != 0;
       return LFFN_OK;
     case LFFN_OPT_GATHER_VARIANT:
-      if (value != 0 && value != -1)
+      if (value != 0 && value != -1 && value != 1)
         return fail(LFFN_ERR_USAGE, "option: no such gather variant " + std::to_string(value));
       c->gather_variant = value;
       return LFFN_OK;
-    case LFFN_OPT_FUSED:
-      if (value < 0 || value > 1) return fail(LFFN_ERR_USAGE, "option: fused must be 0 or 1");
-      c->fused = int(value);
+    case LFFN_OPT_BWD_ONE_PASS:
+      c->bwd_one_pass = value != 0;
+      return LFFN_OK;
+    case LFFN_OPT_HASH_EXACT:
+      c->hash_exact = value != 0;
+      return LFFN_OK;
+    case LFFN_OPT_HOST_CHUNKS:
+      if (value < 1 || value > lffn_ctx::kChunks)
+        return fail(LFFN_ERR_USAGE, "option: host chunks must be 1 .. 16");
+      c->host_chunks = int(value);
       return LFFN_OK;
     case LFFN_OPT_BF16_COEFF_FMA:
       c->bf16w = value != 0;

@@ -302,6 +302,20 @@ class LookupFFN:
             self.upload_tables(tables)
 
     @classmethod
+    def _view(cls, ctx, cfg: LookupConfig, proj, table_range: tuple, *, device: int = 0,
+              max_tokens: int = 65536, table_dtype: str = "f32") -> "LookupFFN":
+        """A non-owning layer over a context another object owns (the shard
+        context of an lffn_group)."""
+        self = cls.__new__(cls)
+        self.cfg, self.proj, self.device = cfg, proj, device
+        self.max_tokens = max_tokens
+        self.table_dtype = _DTYPES[table_dtype]
+        self._ctx = C.c_void_p(ctx)
+        self._owned = False
+        self.table_range = tuple(table_range)
+        return self
+
+    @classmethod
     def from_checkpoint(cls, path: str, *, device: int = 0, max_tokens: int = 65536,
                         table_dtype: str = "f32",
                         table_range: Optional[tuple] = None) -> "LookupFFN":
@@ -324,7 +338,7 @@ class LookupFFN:
     # -- tables ----------------------------------------------------------
     def upload_tables(self, tables) -> None:
         """Upload the FULL h x 2^tau x d_out stack (HashTables or ndarray)."""
-        data = tables.data if isinstance(tables, HashTables) else tables
+        data = tables.data if isinstance(tables, (HashTables, TableSlice)) else tables
         if hasattr(data, "detach"):
             data = data.detach().cpu().numpy()
         data = np.ascontiguousarray(data)
@@ -471,14 +485,18 @@ class LookupFFN:
     def set_option(self, name: str, value: int) -> None:
         """'dense_exact' (exact float64 dense projection instead of the
         tcgen05 split-precision GEMM), 'table_group_bytes', 'gather_variant'
-        (0 default, -1 one warp per token always), 'fused' (1 = the opt-in
-        one-kernel hash + gather) or 'bf16_coeff_fma' (0 = never take the
-        exact mixed-precision FMA path for bf16 tables)."""
+        (0 default, -1 one warp per token always), 'bf16_coeff_fma' (0 =
+        never take the exact mixed-precision FMA path for bf16 tables),
+        'bwd_one_pass' (single-pass backward table-row dot), 'hash_exact' (1 =
+        the signflip hash always in the reference's stage order, z
+        bit-identical) or 'host_chunks' (forward_host pipeline chunks)."""
         opt = {"dense_exact": _capi.LFFN_OPT_DENSE_EXACT,
                "table_group_bytes": _capi.LFFN_OPT_TABLE_GROUP_BYTES,
                "gather_variant": _capi.LFFN_OPT_GATHER_VARIANT,
-               "fused": _capi.LFFN_OPT_FUSED,
-               "bf16_coeff_fma": _capi.LFFN_OPT_BF16_COEFF_FMA}[name]
+               "bf16_coeff_fma": _capi.LFFN_OPT_BF16_COEFF_FMA,
+               "bwd_one_pass": _capi.LFFN_OPT_BWD_ONE_PASS,
+               "hash_exact": _capi.LFFN_OPT_HASH_EXACT,
+               "host_chunks": _capi.LFFN_OPT_HOST_CHUNKS}[name]
         check(_capi.lib().lffn_ctx_set_option(self._ctx, opt, int(value)))
 
     def launch_count(self) -> int:
@@ -494,7 +512,8 @@ class LookupFFN:
 
     def close(self) -> None:
         if getattr(self, "_ctx", None):
-            _capi.lib().lffn_ctx_destroy(self._ctx)
+            if getattr(self, "_owned", True):
+                _capi.lib().lffn_ctx_destroy(self._ctx)
             self._ctx = None
 
     def __del__(self):

@@ -36,6 +36,10 @@ from typing import Callable, Optional, Tuple
 import torch
 import torch.distributed as dist
 
+import ctypes as C
+
+from . import _capi
+from ._capi import check
 from .lookup import HashTables, LookupConfig, LookupFFN, Projection
 
 PartialFn = Callable[[torch.Tensor, torch.Tensor], None]
@@ -222,3 +226,64 @@ class _RowGather:
 
     def __call__(self, xr, out, rows):
         self.fn(self.codes[rows], self.coeff[rows], out)
+
+
+class NativeTableShard:
+    """One rank of the table-sharded forward through the C-ABI lffn_group
+    (include/lffn_gpu.h): the group owns its NCCL communicator, the rank's
+    table shard and the token-block hash context; lffn_forward_sharded does
+    hash -> record exchange -> chunked gather + NCCL combine with no torch on
+    the data path.  A C++ caller of the reference uses the same four calls
+    (INTEGRATION.md).  ``nccl_id``: 128 bytes from ``unique_id()`` on rank 0,
+    shared by any means (here: torch.distributed.broadcast_object_list)."""
+
+    COMBINES = {"reduce_scatter": _capi.LFFN_COMBINE_REDUCE_SCATTER,
+                "all_reduce": _capi.LFFN_COMBINE_ALL_REDUCE,
+                "none": _capi.LFFN_COMBINE_NONE}
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check(_capi.lib().lffn_nccl_unique_id(buf, 128))
+        return buf.raw
+
+    def __init__(self, cfg: LookupConfig, proj: Projection, tables, *, rank: int, world: int,
+                 nccl_id: bytes, device: int = 0, max_tokens: int = 65536,
+                 table_dtype: str = "f32", chunks: int = 4):
+        L = _capi.lib()
+        g = C.c_void_p()
+        idbuf = C.create_string_buffer(bytes(nccl_id), 128)
+        check(L.lffn_group_create(C.byref(g), device, max_tokens, C.byref(cfg._c()),
+                                  C.byref(proj._c()), idbuf, rank, world))
+        self._g = g
+        self.cfg, self.rank, self.world = cfg, rank, world
+        self.table_range = split_range(cfg.tables, world, rank)
+        check(L.lffn_group_set_chunks(g, int(chunks)))
+        self.chunks = int(chunks)
+        self.layer = LookupFFN._view(L.lffn_group_shard(g), cfg, proj, self.table_range,
+                                     device=device, max_tokens=max_tokens,
+                                     table_dtype=table_dtype)
+        if tables is not None:
+            self.layer.upload_tables(tables)
+
+    def forward(self, x: torch.Tensor, out: Optional[torch.Tensor] = None,
+                combine: str = "reduce_scatter", stream=None) -> torch.Tensor:
+        n = x.shape[0]
+        rows = n // self.world if combine == "reduce_scatter" else n
+        y = out if out is not None else x.new_empty((rows, self.cfg.d_out))
+        st = torch.cuda.current_stream().cuda_stream if stream is None else int(stream)
+        check(_capi.lib().lffn_forward_sharded(self._g, x.data_ptr(), n, y.data_ptr(),
+                                               self.COMBINES[combine], st))
+        return y
+
+    def close(self) -> None:
+        if getattr(self, "_g", None):
+            self.layer.close()
+            _capi.lib().lffn_group_destroy(self._g)
+            self._g = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

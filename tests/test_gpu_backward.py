@@ -17,6 +17,7 @@ from gpu_helpers import assert_close, stored_tables, to_oracle
 from paper_2403_07221_b200 import (HashTables, LookupConfig, LookupFFN, LookupVariant,
                                    NumericError, Projection, ProjectionSpec, ProjKind, SizeError,
                                    fill_gaussian, gaussian_matrix)
+from paper_2403_07221_b200.configs import WORKLOADS, make_params, make_x
 
 pytestmark = pytest.mark.gpu
 
@@ -156,21 +157,24 @@ def test_backward_non_finite_grad_y_raises():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("name", ["c2", "c2_bf16"])
-def test_two_pass_kb1_bit_identical_to_one_pass(tmp_path, name):
+def test_two_pass_kb1_bit_identical_to_one_pass(name):
     """The default backward (gdot pass with the transposed float64 butterfly,
     per-(token, table) gz pass, four-row table-gradient walk) against the
-    single-pass KB1 (LFFN_BWD_ONE_PASS=1, read once per process): grad_x and
-    grad_T bit-identical."""
-    import os
-    import subprocess
-    import sys
+    single-pass KB1 (option bwd_one_pass): grad_x and grad_T bit-identical."""
+    import torch
 
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    tool = os.path.join(root, "tools", "bwd_ab_check.py")
-    for tag, env in (("a", {"LFFN_BWD_ONE_PASS": "1"}), ("b", {})):
-        subprocess.run([sys.executable, tool, name, str(tmp_path / tag)], check=True,
-                       env={**os.environ, **env}, timeout=600)
-    for suffix in (".npy", "_T.npy"):
-        a = np.load(str(tmp_path / ("a" + suffix)))
-        b = np.load(str(tmp_path / ("b" + suffix)))
-        assert np.array_equal(a, b), suffix
+    w = WORKLOADS[name]
+    cfg, proj, T = make_params(w, ProjKind.signflip)
+    n = 2048
+    layer = LookupFFN(cfg, proj, T, max_tokens=n, table_dtype=w.table_dtype)
+    xd = torch.from_numpy(make_x(w, n)).cuda()
+    g = torch.Generator().manual_seed(3)
+    gy = torch.randn((n, cfg.d_out), generator=g).cuda()
+    outs = []
+    for one in (1, 0):
+        layer.set_option("bwd_one_pass", one)
+        o = layer.backward(xd, gy)
+        layer.sync()
+        outs.append((o["grad_x"].cpu().numpy(), o["grad_tables"].cpu().numpy()))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1], outs[1][1])

@@ -424,27 +424,6 @@ def test_split_gather_matches_single_warp_walk(oracle, name, n):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name,n", [("c2", 4096), ("c2_bf16", 4100), ("c3", 4096)])
-def test_fused_ws_kernel_matches_two_kernels(oracle, name, n):
-    """LFFN_OPT_FUSED = 1 (warp-specialised hash + gather in one kernel): the
-    same records and the same ascending table walk as hash + gather, so y is
-    identical up to the bf16 gather's reversed-round order, and within the
-    north-star tolerance of the oracle."""
-    w = WORKLOADS[name]
-    cfg, proj, T = make_params(w)
-    x = make_x(w, n)
-    layer = LookupFFN(cfg, proj, T, max_tokens=n, table_dtype=w.table_dtype)
-    y2 = device_forward(layer, x)
-    layer.set_option("fused", 1)
-    y1 = device_forward(layer, x)
-    assert np.abs(y1 - y2).max() <= 1e-6 * np.abs(y2).max()
-    c, s = to_oracle(cfg, proj)
-    y_ref = oracle.lookup_forward(c, s, proj.blob, stored_tables(T.data, w.table_dtype),
-                                  x.astype(np.float64))
-    assert_close(y1, y_ref, FP32_TOL, "fused vs oracle")
-
-
-@pytest.mark.gpu
 @pytest.mark.parametrize("name,n", [("c2_bf16", 3000), ("c2_bf16", 40), ("c3", 2500)])
 def test_bf16_coeff_fma_path_bit_identical(name, n):
     """bf16 tables: groups of four tables whose coefficients are bf16 values
@@ -476,3 +455,59 @@ def test_bf16_coeff_fma_path_bit_identical(name, n):
             outs.append(y.cpu().numpy())
     assert np.array_equal(outs[0], outs[2])
     assert np.array_equal(outs[1], outs[3])
+
+
+K1F_SHAPES = [
+    # d_in, d_out, h, tau, n   (D = 2048 / 4096: the production signflip hash)
+    (768, 768, 256, 8, 4096),     # c2
+    (1024, 1024, 128, 10, 2000),  # c3: h*tau = 1280 < D, tables straddle sign words
+    (4096, 64, 512, 8, 300),      # c4 width (two warps per token)
+    (100, 16, 256, 8, 77),        # d_in far below D, ragged n
+    (770, 32, 200, 7, 50),        # d_in % 4 != 0 (scalar x loads), tau 7
+    (2048, 32, 91, 22, 40),       # tau 22 spanning words, h*tau = 2002
+    (3000, 8, 100, 24, 33),       # D = 4096, d_in % 64 != 0
+]
+
+
+@pytest.mark.parametrize("shape", K1F_SHAPES, ids=lambda s: "x".join(map(str, s)))
+def test_production_signflip_hash(oracle, shape):
+    """K1f (hash_sf_kernel.cuh, reordered transform stages): codes bit-exact
+    wherever every |z_ref| of the table exceeds 1e-5 (the north star's bar;
+    in practice everywhere), coefficients within 2.5e-7 of the oracle's
+    top-1 weight, and identical records to the exact kernel (option
+    hash_exact) wherever z is not within 1e-5 of zero -- also for a table
+    shard with an odd start."""
+    from test_gpu_parity_configs import assert_codes_match
+
+    d_in, d_out, h, tau, n = shape
+    cfg = LookupConfig(d_in=d_in, d_out=d_out, tables=h, code_bits=tau)
+    proj = Projection.init(ProjectionSpec(d_in, h * tau, ProjKind.signflip), 1)
+    x = gaussian_matrix(n, d_in, 0).astype(np.float32)
+    x[1] *= 1e-30  # a tiny token: many small |z| (weights below 1)
+    layer = LookupFFN(cfg, proj, None, max_tokens=n)
+    codes, coeff, _ = device_hash(layer, x, want_z=False)
+    c, s = to_oracle(cfg, proj)
+    z_ref = oracle.proj_forward(s, proj.blob, x.astype(np.float64))
+    codes_ref = assert_codes_match(codes, z_ref, h, tau, "K1f")
+    _, absz = oracle.compute_codes(z_ref, h, tau)
+    w_ref = np.array([oracle.top1_weight(a) for a in absz.reshape(-1, tau)]).reshape(n, h)
+    np.testing.assert_allclose(coeff, w_ref.astype(np.float32), rtol=2.5e-7, atol=0)
+    assert (coeff[1] < 1).any()
+    layer.set_option("hash_exact", 1)
+    codes_x, coeff_x, _ = device_hash(layer, x, want_z=False)
+    assert np.array_equal(codes_x, codes_ref)
+    kb, ke = h // 3 + 1, h - 1
+    sh = LookupFFN(cfg, proj, None, max_tokens=n, table_range=(kb, ke))
+    codes_s, coeff_s, _ = device_hash(sh, x, want_z=False)
+    assert np.array_equal(codes_s, codes[:, kb:ke])
+    assert np.array_equal(coeff_s, coeff[:, kb:ke])
+
+
+def test_production_signflip_hash_non_finite_input():
+    cfg = LookupConfig(d_in=768, d_out=8, tables=256, code_bits=8)
+    proj = Projection.init(ProjectionSpec(768, 2048, ProjKind.signflip), 1)
+    x = gaussian_matrix(64, 768, 0).astype(np.float32)
+    x[40, 700] = np.inf
+    layer = LookupFFN(cfg, proj, None, max_tokens=64)
+    with pytest.raises(NumericError, match="projection forward input"):
+        device_hash(layer, x, want_z=False)

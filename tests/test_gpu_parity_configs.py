@@ -99,7 +99,7 @@ def test_c5_full_size_skewed(oracle):
 def test_c4_table_sharded_all_reduce_world1(oracle):
     """c4 through ShardedLookupFFN(combine = "all_reduce") on a world-1 NCCL
     group (the north star's c4 multi-GPU path): y equals the plain forward
-    bit for bit and the oracle within the bar."""
+    up to fp32 reassociation and the oracle within the bar."""
     import socket
 
     import torch
@@ -119,9 +119,11 @@ def test_c4_table_sharded_all_reduce_world1(oracle):
     try:
         sh = ShardedLookupFFN(cfg, proj, T, mode="table", combine="all_reduce", device=0,
                               max_tokens=n, chunks=4, table_dtype="bf16")
-        y = sh.forward(torch.from_numpy(x).cuda())
+        y = sh.forward(torch.from_numpy(x).cuda()).cpu().numpy()
         torch.cuda.synchronize()
-        np.testing.assert_array_equal(y.cpu().numpy(), plain)
         sh.close()
+        # the chunks (128 tokens) take the split gather, the plain forward
+        # (512) the one-warp walk: fp32 reassociation only
+        assert np.abs(y - plain).max() <= 1e-6 * np.abs(plain).max()
     finally:
         dist.destroy_process_group()
