@@ -22,17 +22,20 @@
 // Layout: TPT = D / 64 threads own one token, 64 float64 registers each.
 //   A: thread t holds indices 64 t + r            (index bits 0-5 in registers)
 //   B: thread t holds indices t + TPT r          (bits log2(TPT) .. +5 in registers)
-// Transform 0 runs its A bits, transposes A -> B through shared memory and
-// finishes its remaining bits; transform 1 runs all its B bits, transposes
-// B -> A and finishes; transform 2 runs all its A bits, transposes A -> B and
-// finishes.  Three transposes (one 128-bit store + one 64-bit load pass, or
-// the reverse) per token against K1's six stores and five loads; both access
-// patterns are bank-conflict free with two padding doubles per 64.
+// Every transform runs the same code: sign flip, butterflies over the six
+// index bits in the registers, one transpose through shared memory (64-bit
+// stores in the B pattern, 128-bit loads in the A pattern; both bank-conflict
+// free with two padding doubles per 64), butterflies over the bits the
+// transpose brought into the registers.  The stages of a Walsh-Hadamard
+// transform commute, so which bits sit in the registers may differ from
+// transform to transform: x starts in a layout L0 chosen so that three
+// transposes end in layout A (sf_start_index).  Three transposes per token
+// against K1's six stores and five loads.
 //
-// Epilogue in layout B: one warp ballot per register gives 32 consecutive
-// sign bits (z >= 0, lookup.cpp:77), so the h*tau code bits come out as words
-// in shared memory and each thread funnel-shifts its tables' codes out of
-// them.  The weight is exactly 1.0 for a table whose every |z_j| >= 18.5
+// Epilogue in layout A: a thread's 64 registers are 64 consecutive
+// coordinates, so its sign bits (z >= 0, lookup.cpp:77) form two words of the
+// h*tau code bits in shared memory, from which each thread funnel-shifts its
+// tables' codes.  The weight is exactly 1.0 for a table whose every |z_j| >= 18.5
 // (1 + exp(-2|z|) rounds to 1.0); the rare small coordinates (a second
 // ballot) have their z stored, and the table's weight divides by
 // 1 + exp(-2|z_j|) over exactly those j in ascending order -- the reference's
@@ -54,7 +57,7 @@ struct HashSfParams {
   int tau;
   int kb, ke;                  // tables owned: [kb, ke)
   const unsigned long long* masks;  // [3][TPT]: bit r = sign of the element thread t holds in
-                               // register r (layout A for transforms 0 and 2, B for 1)
+                               // register r at the start of transform tr (sf_layout_index)
   uint32_t* codes;             // [n x (ke - kb)]
   float* coeff;                // [n x (ke - kb)]
   int* flag;
@@ -121,6 +124,31 @@ __device__ __forceinline__ void sf_io_B(double* sm, double (&v)[64], int t) {
   }
 }
 
+// Index held by thread t in register r at the start (layout L0).  The
+// transpose (store at index t + TPT r, load index 64 t' + r') maps layout L
+// to L'(t', r') = L(r' mod TPT, (TPT/32) t' ... ) -- for D = 4096 it swaps t
+// and r, for D = 2048 L'(l, r) = L(r & 31, 2 l + (r >> 5)).  L0 is chosen so
+// that three transposes end in layout A (index 64 t + r):
+//   D = 2048: L0 = 1024 (l & 1) + 32 (r >> 1) + 16 (r & 1) + (l >> 1)
+//             L1 = 32 l + 1024 (r & 1) + (r >> 1),  L2 = l + 32 r (= B),  L3 = A
+//   D = 4096: L0 = t + 64 r (= B), L1 = A, L2 = B, L3 = A
+// Each transform's first butterflies cover the six index bits its layout
+// holds in registers, the second ones the register bits that came from the
+// threads (D = 2048: register bits 0-4; D = 4096: all six), i.e. every bit
+// exactly once.  The host builds the sign masks in L0, L1, L2.
+template <int LOGD>
+__host__ __device__ __forceinline__ int sf_start_index(int t, int r) {
+  if constexpr (LOGD == 11) return 1024 * (t & 1) + 32 * (r >> 1) + 16 * (r & 1) + (t >> 1);
+  else return t + 64 * r;
+}
+__host__ __device__ __forceinline__ int sf_layout_index(int logd, int tr, int t, int r) {
+  if (logd == 12) return (tr & 1) ? 64 * t + r : t + 64 * r;
+  if (tr == 0) return sf_start_index<11>(t, r);
+  if (tr == 1) return 32 * t + 1024 * (r & 1) + (r >> 1);
+  if (tr == 2) return t + 32 * r;
+  return 64 * t + r;
+}
+
 __device__ __noinline__ double sf_one_plus_exp_m2(double a) { return __dadd_rn(1.0, exp(-2.0 * a)); }
 
 template <int LOGD>
@@ -133,7 +161,6 @@ __global__ void __launch_bounds__(128, 3) hash_sf_kernel(HashSfParams p) {
   constexpr int SLOT = Gm::PAD + Gm::WORDS;  // doubles (the words take WORDS doubles)
   const int slot = threadIdx.x / TPT;
   const int t = threadIdx.x - slot * TPT;
-  const int lane = threadIdx.x & 31;
   const int64_t token = (int64_t)blockIdx.x * TPB + slot;
   const bool active = token < p.n;
   double* sm = smem + (size_t)slot * SLOT;
@@ -146,101 +173,69 @@ __global__ void __launch_bounds__(128, 3) hash_sf_kernel(HashSfParams p) {
   int bad = 0;
   double v[64];
 
-  // ---- transform 0: x (padded to D) in layout A
+  // ---- x (padded to D) into the start layout L0 (below); the finiteness
+  // test rides on an FMA chain (x * 0 is NaN iff x is inf / NaN)
   {
     const float* xr = p.x + token * (int64_t)p.d_in;
-    const int a0 = 64 * t;
-    if (a0 + 64 <= p.d_in && (p.d_in & 3) == 0) {
+    float nanacc = 0.f;
 #pragma unroll
-      for (int r = 0; r < 64; r += 4) {
-        const float4 f = __ldg(reinterpret_cast<const float4*>(xr + a0 + r));
-        if (!isfinite(f.x) || !isfinite(f.y) || !isfinite(f.z) || !isfinite(f.w)) bad |= 1;
-        v[r] = (double)f.x;
-        v[r + 1] = (double)f.y;
-        v[r + 2] = (double)f.z;
-        v[r + 3] = (double)f.w;
+    for (int g = 0; g < 64; g += 16) {
+      float f[16];
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const int a = sf_start_index<LOGD>(t, g + r);
+        f[r] = a < p.d_in ? __ldg(xr + a) : 0.f;
       }
-    } else if (a0 >= p.d_in) {
 #pragma unroll
-      for (int r = 0; r < 64; ++r) v[r] = 0.0;
-    } else {
-#pragma unroll
-      for (int r = 0; r < 64; ++r) {
-        double xv = 0.0;
-        if (a0 + r < p.d_in) {
-          const float f = __ldg(xr + a0 + r);
-          if (!isfinite(f)) bad |= 1;
-          xv = (double)f;
-        }
-        v[r] = xv;
+      for (int r = 0; r < 16; ++r) {
+        nanacc = fmaf(f[r], 0.f, nanacc);
+        v[g + r] = (double)f[r];
       }
     }
+    if (nanacc != nanacc) bad |= 1;
   }
-  sf_flip(v, __ldg(p.masks + 0 * TPT + t));
-  sf_stages<0, 6>(v);
-  sf_io_A<LOGD, true>(sm, v, t);
-  token_sync();
-  sf_io_B<LOGD, false>(sm, v, t);
-  token_sync();
-  // B holds index bits LOGT .. LOGT+5; bit 5 is done when LOGT == 5
-  sf_stages<(LOGD == 11 ? 1 : 0), 6>(v);
-  // ---- transform 1 in layout B
-  sf_flip(v, __ldg(p.masks + 1 * TPT + t));
-  sf_stages<0, 6>(v);
-  sf_io_B<LOGD, true>(sm, v, t);
-  token_sync();
-  sf_io_A<LOGD, false>(sm, v, t);
-  token_sync();
-  sf_stages<0, (LOGD == 11 ? 5 : 6)>(v);
-  // ---- transform 2 in layout A
-  sf_flip(v, __ldg(p.masks + 2 * TPT + t));
-  sf_stages<0, 6>(v);
-  sf_io_A<LOGD, true>(sm, v, t);
-  token_sync();
-  sf_io_B<LOGD, false>(sm, v, t);
-  token_sync();
-  sf_stages<(LOGD == 11 ? 1 : 0), 6>(v);
+  // Three transforms with the same code: sign flip, butterflies over the six
+  // register bits, the transpose (store in the B pattern, load in the A
+  // pattern: it moves the value of thread / register (r' mod T, T' (...))
+  // -- see sf_start_index), butterflies over the register bits the
+  // transpose brought in from the threads.  The transpose permutes which
+  // index bits sit in the registers so that every transform covers each of
+  // its log2(D) bits exactly once, and three of them take the start layout
+  // L0 to layout A.  The loop is not unrolled: one copy of the butterfly code
+  // (the kernel stays within the 32 KB L1.5 instruction cache).
+#pragma unroll 1
+  for (int tr = 0; tr < 3; ++tr) {
+    sf_flip(v, __ldg(p.masks + tr * TPT + t));
+    sf_stages<0, 6>(v);
+    sf_io_B<LOGD, true>(sm, v, t);
+    token_sync();
+    sf_io_A<LOGD, false>(sm, v, t);
+    token_sync();
+    sf_stages<0, (LOGD == 11 ? 5 : 6)>(v);
+  }
 
-  // ---- epilogue in layout B: z[t + TPT r] = v[r]
+  // ---- epilogue in layout A: z[64 t + r] = v[r]
+  // sign bits (z >= 0, lookup.cpp:77), small-|z| bits (|z| < 18.5) and the
   // finiteness of the first h*tau outputs (projection.cpp:264, lookup.cpp:204)
-  {
-    bool fin = true;
-#pragma unroll
-    for (int r = 0; r < 64; ++r)
-      if (t + TPT * r < p.code_width)
-        fin &= (__double2hiint(v[r]) & 0x7ff00000) != 0x7ff00000;
-    if (!fin) bad |= 2;
-  }
-  // sign words (z >= 0, lookup.cpp:77) and small-|z| words (|z| < 18.5):
-  // register r of warp w covers indices 32 (w + (TPT / 32) r) .. + 31
-  const int wsub = t >> 5;          // warp within the token (0 for D = 2048)
-  constexpr int WPT = TPT / 32;     // warps per token
-  uint32_t sw0 = 0, sw1 = 0, mw0 = 0, mw1 = 0;
-  bool any_small = false;
+  uint32_t s0 = 0, s1 = 0, m0 = 0, m1 = 0;
+  bool fin = true;
 #pragma unroll
   for (int r = 0; r < 64; ++r) {
-    const uint32_t s = __ballot_sync(0xffffffffu, v[r] >= 0.0);
-    const uint32_t m = __ballot_sync(0xffffffffu, fabs(v[r]) < 18.5);
-    any_small |= m != 0u;
-    if (r < 32) {
-      if (lane == r) { sw0 = s; mw0 = m; }
-    } else {
-      if (lane == r - 32) { sw1 = s; mw1 = m; }
-    }
+    const uint32_t sb = v[r] >= 0.0 ? 1u : 0u;
+    const uint32_t mb = fabs(v[r]) < 18.5 ? 1u : 0u;
+    if (r < 32) { s0 |= sb << r; m0 |= mb << r; }
+    else { s1 |= sb << (r - 32); m1 |= mb << (r - 32); }
+    if (64 * t + r < p.code_width) fin &= (__double2hiint(v[r]) & 0x7ff00000) != 0x7ff00000;
   }
-  // word index of register r in warp w: WPT * r + w
-  words[WPT * lane + wsub] = sw0;
-  words[WPT * (lane + 32) + wsub] = sw1;
-  words[Gm::WORDS + WPT * lane + wsub] = mw0;
-  words[Gm::WORDS + WPT * (lane + 32) + wsub] = mw1;
-  // the z of every small coordinate (warp-uniform per register: only the
-  // registers some lane flagged), at its natural shared-memory position
-  if (any_small) {
+  if (!fin) bad |= 2;
+  // words 2t, 2t+1 hold indices 64 t .. 64 t + 63
+  reinterpret_cast<uint2*>(words)[t] = make_uint2(s0, s1);
+  reinterpret_cast<uint2*>(words + Gm::WORDS)[t] = make_uint2(m0, m1);
+  // the z of every small coordinate, at its natural shared-memory position
+  if ((m0 | m1) != 0u) {
 #pragma unroll
-    for (int r = 0; r < 64; ++r) {
-      const uint32_t m = __shfl_sync(0xffffffffu, r < 32 ? mw0 : mw1, r & 31);
-      if (m != 0u) sm[Gm::pos(t + TPT * r)] = v[r];
-    }
+    for (int r = 0; r < 64; ++r)
+      if ((((r < 32 ? m0 : m1) >> (r & 31)) & 1u) != 0u) sm[Gm::pos(64 * t + r)] = v[r];
   }
   token_sync();
   const int hl = p.ke - p.kb;

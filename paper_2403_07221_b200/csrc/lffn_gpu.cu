@@ -629,23 +629,11 @@ int launch_gather_group(lffn_ctx* c, const uint32_t* codes, const float* coeff, 
         LFFN_CUDA(cudaGetLastError());
         return LFFN_OK;
       }
-      // Narrow part-major walk (gather_variant 1): one 256-column (bf16) /
-      // 128-column (fp32) chunk per warp, 8 tables in flight per lane, 4
-      // (bf16: 3) CTAs per SM, items part-major, so a round of resident warps touches
-      // 1/nchunks of every row -- the working set of a table stack larger
-      // than L2 (c3: 268 MB -> 67 MB per part) stays L2-resident.
-      const bool narrow = c->gather_variant == 1 && nchunks >= 2 && p.nk % 8 == 0 && S == 1;
-      if (narrow) {
-        const int64_t nwarps_n = n * nchunks;
-        const int minb = f32 ? 4 : 3;  // bf16: 85 registers (64 spill)
-        const unsigned ngrid = (unsigned)std::min<int64_t>(int64_t(c->num_sms) * minb, (nwarps_n * 32 + 255) / 256);
-        p.reverse_odd_rounds = 0;
-        if (f32) gather_row_persistent_kernel<float, 1, 8, 4, true><<<ngrid, 256, 0, st>>>(p, nchunks);
-        else gather_row_persistent_kernel<__nv_bfloat16, 1, 8, 3, true><<<ngrid, 256, 0, st>>>(p, nchunks);
-        ++c->launches;
-        LFFN_CUDA(cudaGetLastError());
-        return LFFN_OK;
-      }
+      // (a narrow part-major walk -- one 256-column bf16 / 128-column fp32
+      // chunk per warp, 8 tables in flight, 3-4 CTAs per SM, so a round
+      // touches 1/nchunks of every row and c3's working set fits L2 --
+      // measured slower everywhere: c3 1.39 vs 1.08 ms, c2 0.89 vs 0.65,
+      // c2 bf16 0.46 vs 0.36, c4 2.59 vs 1.76)
       // (measured at c2 fp32: one warp per token with 6 chunks and 2 CTAs/SM
       // beats 2-3 warps per token at 3-4 CTAs/SM, 0.641 vs 0.698-0.942 ms;
       // L2 evict_last/evict_first splits of the table stack: 0.68-0.81 ms)
@@ -908,14 +896,14 @@ int lffn_ctx_create_shard(lffn_ctx** out, int device, int64_t max_tokens, const 
     CK(cudaMemcpy(c->d_signmask, mask.data(), mask.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
     if (D == 2048 || D == 4096) {
       // K1f sign masks in its register layouts (hash_sf_kernel.cuh): thread
-      // t, register r holds index 64 t + r (layout A: transforms 0 and 2) or
-      // t + (D / 64) r (layout B: transform 1)
+      // t, register r holds index sf_layout_index(log2 D, tr, t, r) at the
+      // start of transform tr
       const int64_t tpt = D / 64;
       std::vector<unsigned long long> sf(size_t(3 * tpt), 0ull);
       for (int64_t tr = 0; tr < 3; ++tr)
         for (int64_t t = 0; t < tpt; ++t)
           for (int64_t r = 0; r < 64; ++r) {
-            const int64_t j = tr == 1 ? t + tpt * r : 64 * t + r;
+            const int64_t j = sf_layout_index(D == 2048 ? 11 : 12, int(tr), int(t), int(r));
             if (blob[tr * D + j] == -1.0) sf[size_t(tr * tpt + t)] |= 1ull << r;
           }
       CK(cudaMalloc(&c->d_sfmask, sf.size() * sizeof(unsigned long long)));
@@ -1561,7 +1549,7 @@ int lffn_ctx_set_option(lffn_ctx* c, int option, int64_t value) {
       c->dense_exact = value != 0;
       return LFFN_OK;
     case LFFN_OPT_GATHER_VARIANT:
-      if (value != 0 && value != -1 && value != 1)
+      if (value != 0 && value != -1)
         return fail(LFFN_ERR_USAGE, "option: no such gather variant " + std::to_string(value));
       c->gather_variant = value;
       return LFFN_OK;
