@@ -305,6 +305,15 @@ int lffn_probe_bandwidth(int device, int which, int reps, double* gbs);
 
 /* Thread-local message for the last non-zero status. */
 const char* lffn_last_error(void);
+/* The reference exception class of the last failure on this thread:
+ * status 1 splits into SizeError (shape / size checks, e.g. lookup.cpp:28-36,
+ * 176-181) and UsageError (unknown names, checkpoint I/O, wrong call order)
+ * as the reference throws them (common.hpp:17-23). */
+#define LFFN_CLASS_SIZE 1
+#define LFFN_CLASS_USAGE 2
+#define LFFN_CLASS_NUMERIC 3
+#define LFFN_CLASS_RUNTIME 4
+int lffn_last_error_class(void);
 
 /* Library identification: "lffn_gpu <version> sm_100a". */
 const char* lffn_version(void);

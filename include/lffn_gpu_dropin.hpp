@@ -15,12 +15,18 @@
 // HashTables / LookupConfig and the error types; nothing here depends on the
 // reference's implementation files.  There is no CPU fallback: a missing
 // device surfaces as std::runtime_error, a LookupCache (training) as
-// UsageError, neighbor_count above the device limit (256) as SizeError.
+// UsageError, neighbor_count above the device limit (256) as SizeError; the
+// other validation failures throw SizeError or UsageError exactly where the
+// reference does (lffn_last_error_class).
 #pragma once
 
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "lffn_gpu.h"
@@ -32,12 +38,42 @@
 namespace lffn {
 namespace gpu {
 
+/// Status -> the reference's exception types (common.hpp:13-37): status 1
+/// is SizeError or UsageError as lffn_last_error_class() says, 2 NumericError.
 inline void check(int status) {
   if (status == LFFN_OK) return;
   const std::string msg = lffn_last_error();
-  if (status == LFFN_ERR_USAGE) throw SizeError(msg);
+  if (status == LFFN_ERR_USAGE) {
+    if (lffn_last_error_class() == LFFN_CLASS_SIZE) throw SizeError(msg);
+    throw UsageError(msg);
+  }
   if (status == LFFN_ERR_NUMERIC) throw NumericError(msg);
   throw std::runtime_error("lffn_gpu: " + msg);
+}
+
+/// 64-bit content hash of a float64 array (multi-threaded): the drop-in
+/// reuses its device copy of the tables only while they are unchanged.
+inline uint64_t content_hash(const std::vector<double>& v) {
+  const std::size_t n = v.size();
+  const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  std::vector<uint64_t> part(nt, 0);
+  std::vector<std::thread> th;
+  for (unsigned t = 0; t < nt; ++t)
+    th.emplace_back([&, t] {
+      const std::size_t b = n * t / nt, e = n * (t + 1) / nt;
+      uint64_t h = 0x9e3779b97f4a7c15ull ^ (uint64_t(t) << 32);
+      for (std::size_t i = b; i < e; ++i) {
+        uint64_t u;
+        std::memcpy(&u, &v[i], 8);
+        h = (h ^ u) * 0x100000001b3ull;
+        h ^= h >> 29;
+      }
+      part[t] = h;
+    });
+  for (auto& x : th) x.join();
+  uint64_t h = n;
+  for (uint64_t p : part) h = (h ^ p) * 0x9e3779b97f4a7c15ull;
+  return h;
 }
 
 inline lffn_cfg to_c(const LookupConfig& c) {
@@ -105,6 +141,10 @@ class Layer {
 };
 
 /// Drop-in for lffn::lookup_forward (lookup.hpp:124-125), any neighbor_count <= 256.
+/// The reference call is stateless; the device layer (context, converted
+/// tables) is cached per thread and reused while the configuration, the
+/// projection and the table contents are unchanged (content hashes), and
+/// the batch fits its max_tokens -- repeated calls skip the table upload.
 inline DenseMatrix lookup_forward(const DenseMatrix& x, const Projection& proj,
                                   const HashTables& tables, const LookupConfig& cfg,
                                   LookupCache* cache = nullptr) {
@@ -113,7 +153,26 @@ inline DenseMatrix lookup_forward(const DenseMatrix& x, const Projection& proj,
   if (x.cols != cfg.d_in) throw SizeError("lookup forward: input width mismatch");
   if (proj.spec().d_in != cfg.d_in || proj.spec().d_out != cfg.code_width())
     throw SizeError("lookup forward: projection must map d_in to h*tau");
-  return Layer(proj, tables, cfg, x.rows > 0 ? x.rows : 1).forward(x);
+  struct Cached {
+    std::unique_ptr<Layer> layer;
+    std::size_t max_tokens = 0;
+    uint64_t key[8] = {};
+  };
+  static thread_local Cached c;
+  const uint64_t key[8] = {uint64_t(cfg.d_in), uint64_t(cfg.d_out), uint64_t(cfg.tables),
+                           uint64_t(cfg.code_bits) | (uint64_t(cfg.variant) << 32),
+                           uint64_t(cfg.neighbor_count) | (uint64_t(proj.spec().kind) << 32),
+                           content_hash(proj.blob()), content_hash(tables.data),
+                           uint64_t(tables.data.size())};
+  const std::size_t rows = x.rows > 0 ? x.rows : 1;
+  const bool same = c.layer && std::memcmp(key, c.key, sizeof(key)) == 0;
+  if (!same || rows > c.max_tokens) {
+    c.max_tokens = same ? std::max(rows, c.max_tokens) : rows;
+    c.layer.reset();
+    c.layer.reset(new Layer(proj, tables, cfg, c.max_tokens));
+    std::memcpy(c.key, key, sizeof(key));
+  }
+  return c.layer->forward(x);
 }
 
 }  // namespace gpu

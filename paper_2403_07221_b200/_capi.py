@@ -15,6 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "csrc", "liblffn_gpu.so")
 
 LFFN_OK, LFFN_ERR_USAGE, LFFN_ERR_NUMERIC, LFFN_ERR_RUNTIME = 0, 1, 2, 3
+LFFN_CLASS_SIZE, LFFN_CLASS_USAGE, LFFN_CLASS_NUMERIC, LFFN_CLASS_RUNTIME = 1, 2, 3, 4
 LFFN_F32, LFFN_BF16, LFFN_F64 = 0, 1, 2
 LFFN_OPT_DENSE_EXACT, LFFN_OPT_TABLE_GROUP_BYTES, LFFN_OPT_GATHER_VARIANT = 1, 2, 3
 LFFN_OPT_BF16_COEFF_FMA, LFFN_OPT_BWD_ONE_PASS, LFFN_OPT_HASH_EXACT, LFFN_OPT_HOST_CHUNKS = 5, 6, 7, 8
@@ -75,6 +76,7 @@ SIGNATURES = {
     "lffn_ctx_stage_ms": (C.c_int, [_VP, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "lffn_probe_bandwidth": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]),
     "lffn_last_error": (C.c_char_p, []),
+    "lffn_last_error_class": (C.c_int, []),
     "lffn_version": (C.c_char_p, []),
     "lffn_nccl_unique_id": (C.c_int, [_VP, _I64]),
     "lffn_group_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, _I64, C.POINTER(lffn_cfg),
@@ -111,11 +113,16 @@ class LffnError(Exception):
     """Base of the errors mapped from C-ABI status codes."""
 
 
-class SizeError(LffnError, ValueError):
-    """SizeError / UsageError analog (status 1; common.hpp:17-23)."""
+class ValidationError(LffnError, ValueError):
+    """Status 1: the reference's std::invalid_argument family (common.hpp:17-23)."""
 
 
-UsageError = SizeError
+class SizeError(ValidationError):
+    """SizeError analog: shape / size checks (lffn_last_error_class() == SIZE)."""
+
+
+class UsageError(ValidationError):
+    """UsageError analog: unknown names, checkpoint I/O, wrong call order."""
 
 
 class NumericError(LffnError, ArithmeticError):
@@ -131,7 +138,7 @@ def check(rc: int) -> None:
         return
     msg = lib().lffn_last_error().decode(errors="replace")
     if rc == LFFN_ERR_USAGE:
-        raise SizeError(msg)
+        raise (SizeError if lib().lffn_last_error_class() == LFFN_CLASS_SIZE else UsageError)(msg)
     if rc == LFFN_ERR_NUMERIC:
         raise NumericError(msg)
     raise DeviceError(msg)

@@ -175,6 +175,21 @@ int lffn_ctx_create_from_checkpoint(lffn_ctx** out, int device, int64_t max_toke
       return fail(LFFN_ERR_USAGE, std::string("checkpoint load: truncated file ") + path);
     proj.blob = blob.data();
     if (table_begin == 0 && table_end == 0) table_end = cfg.tables;
+    // the whole file must hold exactly header + blob + tables, as
+    // load_checkpoint requires (checkpoint.cpp:134-136), even though only the
+    // owned slice is read
+    {
+      const size_t per = (size_t(1) << cfg.code_bits) * size_t(cfg.d_out);
+      const long here = std::ftell(f.f);
+      if (here < 0 || std::fseek(f.f, 0, SEEK_END) != 0)
+        return fail(LFFN_ERR_USAGE, std::string("checkpoint load: truncated file ") + path);
+      const long end = std::ftell(f.f);
+      const long long want = (long long)here + (long long)(size_t(cfg.tables) * per * sizeof(double));
+      if (end < want) return fail(LFFN_ERR_USAGE, std::string("checkpoint load: truncated file ") + path);
+      if (end > want) return fail(LFFN_ERR_USAGE, std::string("checkpoint load: trailing bytes in ") + path);
+      if (std::fseek(f.f, here, SEEK_SET) != 0)
+        return fail(LFFN_ERR_USAGE, std::string("checkpoint load: truncated file ") + path);
+    }
     lffn_ctx* ctx = nullptr;
     if (int rc = lffn_ctx_create_shard(&ctx, device, max_tokens, &cfg, &proj, table_begin, table_end))
       return rc;

@@ -67,6 +67,10 @@ class ShardedLookupFFN:
             raise ValueError(f"unknown combine {combine}")
         if hash_mode not in ("token", "replicated"):
             raise ValueError(f"unknown hash_mode {hash_mode}")
+        if mode == "table" and cfg.neighbor_count != 1:
+            # the record exchange and the partial gathers move one record per
+            # (token, table); nc > 1 runs on one GPU (LookupFFN)
+            raise ValueError("table sharding serves neighbor_count 1")
         self.cfg, self.mode, self.combine = cfg, mode, combine
         self.hash_mode = hash_mode if mode == "table" else "replicated"
         self.group = group

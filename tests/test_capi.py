@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 from paper_2403_07221_b200 import (HashTables, LookupConfig, LookupFFN, LookupVariant, Projection,
-                                   ProjectionSpec, ProjKind, SizeError, _capi, fill_gaussian,
+                                   ProjectionSpec, ProjKind, SizeError, UsageError, _capi, fill_gaussian,
                                    fill_signs, gaussian_matrix, lookup_forward, to_bf16_values)
 from paper_2403_07221_b200._capi import DeviceError
 
@@ -143,7 +143,7 @@ def test_lookup_forward_shape_errors_before_device():
     proj = Projection.init(ProjectionSpec.dense(8, 6), 1)
     with pytest.raises(SizeError, match="input width"):
         lookup_forward(np.zeros((2, 7)), proj, T, cfg)
-    with pytest.raises(SizeError, match="LookupCache"):
+    with pytest.raises(UsageError, match="LookupCache"):
         lookup_forward(np.zeros((2, 8)), proj, T, cfg, cache=object())
 
 

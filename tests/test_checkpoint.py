@@ -9,7 +9,7 @@ import pytest
 
 from oracle import ACDC, BH, DENSE, SCALED, SIGNFLIP, Cfg
 from paper_2403_07221_b200 import (HashTables, LookupConfig, LookupFFN, LookupVariant, Projection,
-                                   ProjectionSpec, ProjKind, SizeError, checkpoint_header,
+                                   ProjectionSpec, ProjKind, SizeError, UsageError, checkpoint_header,
                                    fill_gaussian, load_checkpoint, save_checkpoint)
 
 CASES = [
@@ -70,9 +70,9 @@ def test_checkpoint_errors(tmp_path):
     for msg, data in cases.items():
         p = str(tmp_path / (msg.replace(" ", "_") + ".lffn"))
         open(p, "wb").write(data)
-        with pytest.raises(SizeError, match=msg):
+        with pytest.raises(UsageError, match=msg):  # checkpoint.cpp:88-136
             load_checkpoint(p)
-    with pytest.raises(SizeError, match="cannot open"):
+    with pytest.raises(UsageError, match="cannot open"):
         load_checkpoint(str(tmp_path / "missing.lffn"))
     c2, s2, n = checkpoint_header(good)
     assert (c2.tables, s2.kind, n) == (2, ProjKind.signflip, 2 * 8 * 4)
@@ -97,3 +97,19 @@ def test_layer_from_checkpoint_equals_layer_from_memory(tmp_path, dtype):
     ref = LookupFFN(cfg, proj, tables, max_tokens=64, table_dtype=dtype, table_range=(100, 200))
     assert np.array_equal(device_forward(sh, x), device_forward(ref, x))
     os.remove(path)
+
+
+def test_shard_from_checkpoint_checks_the_whole_file(tmp_path):
+    """A table shard reads only its slice, but a truncated or padded file is
+    rejected as load_checkpoint rejects it (checkpoint.cpp:134-136) -- before
+    any device work, so this runs without a GPU."""
+    cfg = LookupConfig(d_in=8, d_out=4, tables=6, code_bits=3)
+    proj = Projection.init(ProjectionSpec.signflip(8, 18), 1)
+    good = str(tmp_path / "good.lffn")
+    save_checkpoint(good, cfg, proj, HashTables.init(cfg, 2))
+    raw = open(good, "rb").read()
+    for msg, data in {"truncated": raw[:-8], "trailing bytes": raw + b"\x00" * 8}.items():
+        p = str(tmp_path / (msg.replace(" ", "_") + ".lffn"))
+        open(p, "wb").write(data)
+        with pytest.raises(UsageError, match=msg):
+            LookupFFN.from_checkpoint(p, max_tokens=4, table_range=(0, 2))
