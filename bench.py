@@ -364,8 +364,13 @@ def run_ours(args):
             for cold in (False, True):
                 ts = []
                 for r in range(60):
+                    # the device is kept busy up to the first event (L2
+                    # flush, or a spin kernel for warm L2) so the interval
+                    # is device time, not the host's launch latency
                     if cold:
                         flush.fill_(r & 0xFF)
+                    else:
+                        torch.cuda._sleep(100000)
                     e0 = torch.cuda.Event(enable_timing=True)
                     e1 = torch.cuda.Event(enable_timing=True)
                     e0.record(stream)

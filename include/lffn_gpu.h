@@ -242,7 +242,11 @@ int lffn_sync(lffn_ctx* ctx, void* stream);
  *                              4096 (reordered stages, codes bit-exact
  *                              wherever |z| > 1e-5) unless z is requested
  *   LFFN_OPT_HOST_CHUNKS       lffn_forward_host pipeline chunks (1 .. 16,
- *                              default 8) */
+ *                              default 8)
+ *   LFFN_OPT_SMALL_MAX_TOKENS  batches of at most this many tokens (<= 64,
+ *                              default 64; 0 = never) run the whole forward
+ *                              in one launch spread over (token, table
+ *                              group) CTAs (signflip, D = 2048, top-1) */
 #define LFFN_OPT_DENSE_EXACT 1
 #define LFFN_OPT_TABLE_GROUP_BYTES 2
 #define LFFN_OPT_GATHER_VARIANT 3
@@ -250,6 +254,7 @@ int lffn_sync(lffn_ctx* ctx, void* stream);
 #define LFFN_OPT_BWD_ONE_PASS 6
 #define LFFN_OPT_HASH_EXACT 7
 #define LFFN_OPT_HOST_CHUNKS 8
+#define LFFN_OPT_SMALL_MAX_TOKENS 10
 int lffn_ctx_set_option(lffn_ctx* ctx, int option, int64_t value);
 
 /* ---- multi-GPU table sharding (north star: tables split

@@ -23,6 +23,7 @@
 #include "hash_bh_kernel.cuh"
 #include "backward_kernels.cuh"
 #include "hash_sf_kernel.cuh"
+#include "small_kernels.cuh"
 #include "lffn_gpu.h"
 #include "lffn_internal.h"
 #include "neighbor_kernels.cuh"
@@ -158,6 +159,8 @@ struct lffn_ctx {
   int hash_exact = 0;            // LFFN_OPT_HASH_EXACT: always K1 (z bit-identical)
   int host_chunks = 8;           // LFFN_OPT_HOST_CHUNKS: lffn_forward_host pipeline chunks
   unsigned long long* d_sfmask = nullptr;  // K1f: per-thread sign masks [3][D/64]
+  int small_max = 64;                // LFFN_OPT_SMALL_MAX_TOKENS: K5 up to this batch size
+  static constexpr int kSmallTokens = 64;
 };
 
 namespace {
@@ -744,9 +747,94 @@ int launch_gather(lffn_ctx* c, const uint32_t* codes, const float* coeff, int64_
   return LFFN_OK;
 }
 
+// K5 (small_kernels.cuh): the whole forward of a small batch in one launch,
+// grid (token, table group); signflip at D = 2048, top-1, 16-byte rows.
+bool small_eligible(const lffn_ctx* c, int64_t n) {
+  if (n < 1 || n > std::min<int64_t>(c->small_max, lffn_ctx::kSmallTokens)) return false;
+  if (c->proj.kind != LFFN_PROJ_SIGNFLIP || c->n_transforms != 3 || c->logD != 11 || c->nc != 1) return false;
+  const int vec = c->t_dtype == LFFN_F32 ? 4 : 8;
+  return c->h_loc > 0 && c->cfg.d_out % vec == 0 && c->cfg.d_out / vec <= 2 * kSmallThreads;
+}
+
+int launch_small(lffn_ctx* c, const float* d_x, int64_t n, float* d_y, int accumulate, cudaStream_t st) {
+  SmallParams q{};
+  q.x = d_x;
+  q.n = n;
+  q.d_in = int(c->cfg.d_in);
+  q.code_width = int(c->code_width);
+  q.tau = int(c->cfg.code_bits);
+  q.kb = int(c->kb);
+  q.ke = int(c->ke);
+  q.scaled = (c->cfg.variant == LFFN_SCALED || c->cfg.variant == LFFN_GELU_TAU1) ? 1 : 0;
+  // G CTAs per token (a cluster): about two CTAs per SM in total, a power of
+  // two <= 16 (<= 8 above four tokens: clusters of 16 measured slower
+  // there), and at most 256 tables per group.  More CTAs per token cut the
+  // rows each CTA walks but repeat the hash: four CTAs per SM measured
+  // slower at n = 32 / 64 (26.6 / 24.6 vs 15.3 / 18.4 us).
+  const int gmax = n <= 4 ? kSmallMaxGroups : kSmallMaxGroups / 2;
+  int G = 1;
+  while (G < gmax && int64_t(2 * G) * n <= int64_t(c->num_sms) * 2) G *= 2;
+  while (G < kSmallMaxGroups && (c->h_loc + G - 1) / G > kSmallMaxTpg) G *= 2;
+  if ((c->h_loc + G - 1) / G > kSmallMaxTpg)
+    return fail(LFFN_ERR_USAGE, "small forward: more than 4096 tables");
+  q.tpg = int((c->h_loc + G - 1) / G);
+  q.groups = G;
+  q.signmask = c->d_signmask;
+  q.T = c->d_T;
+  q.rows = int(c->rows);
+  q.d_out = int(c->cfg.d_out);
+  q.y = d_y;
+  q.accumulate = accumulate;
+  q.flag = c->d_flag;
+  const bool f32 = c->t_dtype == LFFN_F32;
+  const int nch = int(c->cfg.d_out / (f32 ? 4 : 8));
+  using SK = void (*)(SmallParams);
+  SK fn = f32 ? (nch <= kSmallThreads ? &forward_small_kernel<float, 1> : &forward_small_kernel<float, 2>)
+              : (nch <= kSmallThreads ? &forward_small_kernel<__nv_bfloat16, 1>
+                                      : &forward_small_kernel<__nv_bfloat16, 2>);
+  {
+    // clusters of 16 are non-portable: allowed per kernel, per device
+    static std::mutex mu;
+    static bool done[64] = {};
+    std::lock_guard<std::mutex> lock(mu);
+    if (c->device < 64 && !done[c->device]) {
+      for (SK k : {&forward_small_kernel<float, 1>, &forward_small_kernel<float, 2>,
+                   &forward_small_kernel<__nv_bfloat16, 1>, &forward_small_kernel<__nv_bfloat16, 2>})
+        cudaFuncSetAttribute(reinterpret_cast<const void*>(k), cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      done[c->device] = true;
+    }
+  }
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(unsigned(G), unsigned(n));
+  lc.blockDim = dim3(kSmallThreads);
+  lc.dynamicSmemBytes = 0;
+  lc.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = unsigned(G);
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  LFFN_CUDA(cudaLaunchKernelEx(&lc, fn, q));
+  ++c->launches;
+  LFFN_CUDA(cudaGetLastError());
+  return LFFN_OK;
+}
+
 int forward_impl(lffn_ctx* c, const float* d_x, int64_t n, float* d_y, cudaStream_t st) {
   const bool tm = c->timing;
   if (tm) LFFN_CUDA(cudaEventRecord(c->ev_t0, st));
+  if (small_eligible(c, n)) {
+    // one launch: reported as the gather stage
+    if (tm) LFFN_CUDA(cudaEventRecord(c->ev_t1, st));
+    if (int rc = launch_small(c, d_x, n, d_y, 0, st)) return rc;
+    if (tm) {
+      LFFN_CUDA(cudaEventRecord(c->ev_t2, st));
+      c->timed = true;
+    }
+    return LFFN_OK;
+  }
   if (int rc = launch_hash(c, d_x, n, c->d_codes, c->d_coeff, nullptr, st)) return rc;
   if (tm) LFFN_CUDA(cudaEventRecord(c->ev_t1, st));
   if (int rc = launch_gather(c, c->d_codes, c->d_coeff, n, d_y, 0, st)) return rc;
@@ -1194,12 +1282,16 @@ int lffn_forward_host(lffn_ctx* c, const float* h_x, int64_t n, float* h_y) {
     LFFN_CUDA(cudaEventRecord(c->ev_h2d[i], c->s_h2d));
     LFFN_CUDA(cudaStreamWaitEvent(sc, c->ev_h2d[i], 0));
     const int64_t rec = r0 * c->h_loc * c->nc;
-    if (int rc = launch_hash(c, c->d_xbuf + r0 * d_in, r1 - r0, c->d_codes + rec, c->d_coeff + rec,
-                             nullptr, sc))
-      return rc;
-    if (int rc = launch_gather(c, c->d_codes + rec, c->d_coeff + rec, r1 - r0,
-                               c->d_ybuf + r0 * d_out, 0, sc))
-      return rc;
+    if (small_eligible(c, r1 - r0)) {
+      if (int rc = launch_small(c, c->d_xbuf + r0 * d_in, r1 - r0, c->d_ybuf + r0 * d_out, 0, sc)) return rc;
+    } else {
+      if (int rc = launch_hash(c, c->d_xbuf + r0 * d_in, r1 - r0, c->d_codes + rec, c->d_coeff + rec,
+                               nullptr, sc))
+        return rc;
+      if (int rc = launch_gather(c, c->d_codes + rec, c->d_coeff + rec, r1 - r0,
+                                 c->d_ybuf + r0 * d_out, 0, sc))
+        return rc;
+    }
     LFFN_CUDA(cudaEventRecord(c->ev_comp[i], sc));
     LFFN_CUDA(cudaStreamWaitEvent(c->s_d2h, c->ev_comp[i], 0));
     LFFN_CUDA(cudaMemcpyAsync(h_y + r0 * d_out, c->d_ybuf + r0 * d_out,
@@ -1601,6 +1693,10 @@ int lffn_ctx_set_option(lffn_ctx* c, int option, int64_t value) {
       return LFFN_OK;
     case LFFN_OPT_HASH_EXACT:
       c->hash_exact = value != 0;
+      return LFFN_OK;
+    case LFFN_OPT_SMALL_MAX_TOKENS:
+      if (value < 0) return fail(LFFN_ERR_USAGE, "option: negative small-batch limit");
+      c->small_max = int(std::min<int64_t>(value, lffn_ctx::kSmallTokens));
       return LFFN_OK;
     case LFFN_OPT_HOST_CHUNKS:
       if (value < 1 || value > lffn_ctx::kChunks)

@@ -489,14 +489,16 @@ class LookupFFN:
         never take the exact mixed-precision FMA path for bf16 tables),
         'bwd_one_pass' (single-pass backward table-row dot), 'hash_exact' (1 =
         the signflip hash always in the reference's stage order, z
-        bit-identical) or 'host_chunks' (forward_host pipeline chunks)."""
+        bit-identical), 'host_chunks' (forward_host pipeline chunks) or
+        'small_max_tokens' (one-launch forward for batches up to this size)."""
         opt = {"dense_exact": _capi.LFFN_OPT_DENSE_EXACT,
                "table_group_bytes": _capi.LFFN_OPT_TABLE_GROUP_BYTES,
                "gather_variant": _capi.LFFN_OPT_GATHER_VARIANT,
                "bf16_coeff_fma": _capi.LFFN_OPT_BF16_COEFF_FMA,
                "bwd_one_pass": _capi.LFFN_OPT_BWD_ONE_PASS,
                "hash_exact": _capi.LFFN_OPT_HASH_EXACT,
-               "host_chunks": _capi.LFFN_OPT_HOST_CHUNKS}[name]
+               "host_chunks": _capi.LFFN_OPT_HOST_CHUNKS,
+               "small_max_tokens": _capi.LFFN_OPT_SMALL_MAX_TOKENS}[name]
         check(_capi.lib().lffn_ctx_set_option(self._ctx, opt, int(value)))
 
     def launch_count(self) -> int:

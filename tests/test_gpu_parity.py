@@ -511,3 +511,45 @@ def test_production_signflip_hash_non_finite_input():
     layer = LookupFFN(cfg, proj, None, max_tokens=64)
     with pytest.raises(NumericError, match="projection forward input"):
         device_hash(layer, x, want_z=False)
+
+
+@pytest.mark.parametrize("name,n", [("c5", 1), ("c5", 8), ("c5", 64), ("c2", 3), ("c2_bf16", 17),
+                                    ("c3", 40), ("c2", 64)])
+def test_small_batch_one_launch(oracle, name, n):
+    """K5 (small_kernels.cuh, one launch over (token, table group) CTAs):
+    within the fp32 bar of the oracle on the device's own records, equal to
+    the two-kernel path up to fp32 reassociation, through the device and the
+    host entry points, and for a table shard."""
+    import torch
+
+    from test_gpu_parity_configs import assert_codes_match
+
+    w = WORKLOADS[name]
+    cfg, proj, T = make_params(w)
+    x = make_x(w, n)
+    layer = LookupFFN(cfg, proj, T, max_tokens=max(n, 64), table_dtype=w.table_dtype)
+    y1 = device_forward(layer, x)            # one launch (n <= 64)
+    y_host = layer.forward(x)
+    layer.set_option("small_max_tokens", 0)
+    y2 = device_forward(layer, x)            # hash + gather kernels
+    codes, coeff, _ = device_hash(layer, x, want_z=False)
+    assert np.abs(y1 - y2).max() <= 1e-6 * np.abs(y2).max()
+    assert np.array_equal(y1, y_host)
+    c, s = to_oracle(cfg, proj)
+    z_ref = oracle.proj_forward(s, proj.blob, x.astype(np.float64))
+    assert_codes_match(codes, z_ref, w.h, w.tau, "small")
+    y_ref = oracle.gather(stored_tables(T.data, w.table_dtype), w.h, 1 << w.tau, w.d, codes,
+                          coeff.astype(np.float64))
+    assert_close(y1, y_ref, FP32_TOL, f"{name} n={n} one launch vs oracle")
+    # table shard with an odd start: the partial over its tables
+    kb, ke = 37, w.h - 5
+    sh = LookupFFN(cfg, proj, T, max_tokens=64, table_dtype=w.table_dtype, table_range=(kb, ke))
+    ys = device_forward(sh, x)
+    ys_ref = oracle.gather(stored_tables(T.data, w.table_dtype)[kb * (1 << w.tau) * w.d:
+                                                                ke * (1 << w.tau) * w.d],
+                           ke - kb, 1 << w.tau, w.d, np.ascontiguousarray(codes[:, kb:ke]),
+                           coeff[:, kb:ke].astype(np.float64))
+    assert_close(ys, ys_ref, FP32_TOL, "small shard")
+    # repeated calls reuse the per-token tickets
+    for _ in range(3):
+        assert np.array_equal(device_forward(sh, x), ys)
