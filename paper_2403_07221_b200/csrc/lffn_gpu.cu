@@ -161,6 +161,14 @@ struct lffn_ctx {
   unsigned long long* d_sfmask = nullptr;  // K1f: per-thread sign masks [3][D/64]
   int small_max = 64;                // LFFN_OPT_SMALL_MAX_TOKENS: K5 up to this batch size
   static constexpr int kSmallTokens = 64;
+  // host path of small batches: one CUDA graph per batch size (H2D, K5, D2H,
+  // flag read + reset), its two host pointers patched per call
+  struct HostGraph {
+    cudaGraphExec_t exec = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphNode_t h2d = nullptr, d2h = nullptr;
+  };
+  HostGraph host_graph[kSmallTokens + 1];
 };
 
 namespace {
@@ -212,6 +220,10 @@ void destroy_ctx(lffn_ctx* c) {
   cudaFree(c->d_wnorm);
   cudaFree(c->d_fix_count);
   cudaFree(c->d_sfmask);
+  for (auto& hg : c->host_graph) {
+    if (hg.exec) cudaGraphExecDestroy(hg.exec);
+    if (hg.graph) cudaGraphDestroy(hg.graph);
+  }
   cudaFree(c->d_zbuf);
   cudaFree(c->d_gzbuf);
   cudaFree(c->d_bwd_offs);
@@ -1128,6 +1140,9 @@ int lffn_ctx_create_shard(lffn_ctx** out, int device, int64_t max_tokens, const 
     CK(cudaMalloc(&c->d_zbuf, mt * size_t(c->code_width) * sizeof(double)));
   CK(cudaMalloc(&c->d_flag, sizeof(int)));
   CK(cudaMemset(c->d_flag, 0, sizeof(int)));
+  // lffn_forward_host staging (no allocation on any forward path)
+  CK(cudaMalloc(&c->d_xbuf, mt * size_t(cfg->d_in) * sizeof(float)));
+  CK(cudaMalloc(&c->d_ybuf, mt * size_t(cfg->d_out) * sizeof(float)));
   CK(cudaMallocHost(&c->h_flag, sizeof(int)));
   CK(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking));
@@ -1252,18 +1267,89 @@ int lffn_forward(lffn_ctx* c, const float* d_x, int64_t n, float* d_y, void* str
   return forward_impl(c, d_x, n, d_y, static_cast<cudaStream_t>(stream));
 }
 
+}  // extern "C"
+
+namespace {
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// Small batches through the host path: the whole call (x in, K5, y out, the
+// non-finite flag read and reset) is one CUDA graph per batch size, built on
+// first use; later calls patch the two host pointers and launch it.
+int forward_host_graph(lffn_ctx* c, const float* h_x, int64_t n, float* h_y) {
+  lffn_ctx::HostGraph& hg = c->host_graph[n];
+  const size_t xb = size_t(n) * size_t(c->cfg.d_in) * sizeof(float);
+  const size_t yb = size_t(n) * size_t(c->cfg.d_out) * sizeof(float);
+  cudaStream_t st = c->s_comp;
+  if (!hg.exec) {
+    cudaGraph_t graph = nullptr;
+    const int64_t launches0 = c->launches;  // the capture launches nothing
+    LFFN_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    cudaMemcpyAsync(c->d_xbuf, h_x, xb, cudaMemcpyHostToDevice, st);
+    const int rc = launch_small(c, c->d_xbuf, n, c->d_ybuf, 0, st);
+    cudaMemcpyAsync(h_y, c->d_ybuf, yb, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaMemsetAsync(c->d_flag, 0, sizeof(int), st);
+    const cudaError_t ce = cudaStreamEndCapture(st, &graph);
+    c->launches = launches0;
+    if (rc != LFFN_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return rc;
+    }
+    if (ce != cudaSuccess) return fail(LFFN_ERR_RUNTIME, std::string("host graph capture: ") + cudaGetErrorString(ce));
+    size_t nn = 0;
+    cudaGraphGetNodes(graph, nullptr, &nn);
+    std::vector<cudaGraphNode_t> nodes(nn);
+    cudaGraphGetNodes(graph, nodes.data(), &nn);
+    for (cudaGraphNode_t nd : nodes) {
+      cudaGraphNodeType ty;
+      cudaGraphNodeGetType(nd, &ty);
+      if (ty != cudaGraphNodeTypeMemcpy) continue;
+      cudaMemcpy3DParms mp{};
+      cudaGraphMemcpyNodeGetParams(nd, &mp);
+      if (mp.kind == cudaMemcpyHostToDevice) hg.h2d = nd;
+      else if (mp.dstPtr.ptr == static_cast<void*>(h_y)) hg.d2h = nd;
+    }
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+    if (ie != cudaSuccess || !hg.h2d || !hg.d2h) {
+      if (exec) cudaGraphExecDestroy(exec);
+      cudaGraphDestroy(graph);
+      hg = lffn_ctx::HostGraph{};
+      return fail(LFFN_ERR_RUNTIME, "host graph: instantiation failed");
+    }
+    hg.exec = exec;
+    hg.graph = graph;  // kept: its node handles address the exec's copies
+    // the captured copies were not executed: run this call through the graph
+  }
+  // this call's host pointers into the two copies (nodes of the kept graph)
+  LFFN_CUDA(cudaGraphExecMemcpyNodeSetParams1D(hg.exec, hg.h2d, c->d_xbuf, h_x, xb, cudaMemcpyHostToDevice));
+  LFFN_CUDA(cudaGraphExecMemcpyNodeSetParams1D(hg.exec, hg.d2h, h_y, c->d_ybuf, yb, cudaMemcpyDeviceToHost));
+  ++c->launches;  // K5 inside the graph
+  LFFN_CUDA(cudaGraphLaunch(hg.exec, st));
+  LFFN_CUDA(cudaStreamSynchronize(st));
+  return flag_message(*c->h_flag);
+}
+
+}  // namespace
+
+extern "C" {
+
 int lffn_forward_host(lffn_ctx* c, const float* h_x, int64_t n, float* h_y) {
   if (!c) return fail(LFFN_ERR_USAGE, "null context");
   if (int rc = check_n(c, n)) return rc;
   if (n > 0 && (!h_x || !h_y)) return fail(LFFN_ERR_USAGE, "forward: null buffer");
   if (!c->d_T) return fail(LFFN_ERR_USAGE, "lookup forward: tables not uploaded");
   DeviceGuard g(c->device);
-  if (!c->d_xbuf) {
-    // first host-path call: I/O staging sized for max_tokens (allocated once)
-    LFFN_CUDA(cudaMalloc(&c->d_xbuf, size_t(std::max<int64_t>(c->max_tokens, 1)) * c->cfg.d_in * sizeof(float)));
-    LFFN_CUDA(cudaMalloc(&c->d_ybuf, size_t(std::max<int64_t>(c->max_tokens, 1)) * c->cfg.d_out * sizeof(float)));
-  }
   if (n == 0) return LFFN_OK;
+  if (small_eligible(c, n) && is_pinned(h_x) && is_pinned(h_y)) return forward_host_graph(c, h_x, n, h_y);
   // Chunked pipeline: H2D(chunk i+1) || compute(chunk i) || D2H(chunk i-1).
   // Structured projections use no context scratch, so consecutive chunks
   // alternate between two compute streams and their kernels overlap (one
