@@ -35,8 +35,15 @@ cfg, proj, T = make_params(w, ProjKind.signflip)
 layer = LookupFFN(cfg, proj, T, max_tokens=n)
 x = torch.from_numpy(make_x(w, n)).pin_memory()
 y = torch.empty((n, 768), dtype=torch.float32).pin_memory()
-ms = timeit(lambda: layer.forward_host_ptr(x.data_ptr(), n, y.data_ptr()))
-print(f"forward_host chunks={os.environ.get('LFFN_HOST_CHUNKS', 8)}: {ms:.3f} ms  {n/ms*1e3/1e6:.2f} M tok/s")
+for ch in (4, 6, 8, 10, 12, 16):
+    layer.set_option("host_chunks", ch)
+    ms = timeit(lambda: layer.forward_host_ptr(x.data_ptr(), n, y.data_ptr()))
+    print(f"forward_host chunks={ch}: {ms:.3f} ms  {n/ms*1e3/1e6:.2f} M tok/s")
+layer.set_option("host_chunks", 8)
+xp = make_x(w, n)
+yp = np.empty((n, 768), np.float32)
+ms = timeit(lambda: layer.forward(xp, yp))
+print(f"forward_host pageable numpy buffers: {ms:.3f} ms  {n/ms*1e3/1e6:.2f} M tok/s")
 xd = x.cuda()
 yd = torch.empty((n, 768), dtype=torch.float32, device="cuda")
 for nchunk in (1, 4, 8, 16):
