@@ -358,6 +358,7 @@ def run_ours(args):
     # L2 and after an L2 flush, and through the host path
     small = None
     if args.config == "c5" and mode == "token":
+        layer.set_timing(False)  # no stage events inside the measured calls
         small = {}
         for m in (1, 8, 64):
             res = {}

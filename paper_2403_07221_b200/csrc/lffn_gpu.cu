@@ -671,11 +671,13 @@ int launch_gather_group(lffn_ctx* c, const uint32_t* codes, const float* coeff, 
         LFFN_CUDA(cudaGetLastError());
         return LFFN_OK;
       }
-      // (a narrow part-major walk -- one 256-column bf16 / 128-column fp32
-      // chunk per warp, 8 tables in flight, 3-4 CTAs per SM, so a round
-      // touches 1/nchunks of every row and c3's working set fits L2 --
-      // measured slower everywhere: c3 1.39 vs 1.08 ms, c2 0.89 vs 0.65,
-      // c2 bf16 0.46 vs 0.36, c4 2.59 vs 1.76)
+      // (a narrow part-major walk -- one 16-byte chunk per lane, so a round
+      // of resident warps touches 1/nchunks of every row and c3's 268 MB
+      // stack fits L2 per part -- measured slower everywhere, with 8 tables
+      // in flight at 3-4 CTAs per SM (c3 1.39 vs 1.08 ms, c4 2.59 vs 1.76)
+      // and with 16 at 2 CTAs per SM (c3 1.46 vs 1.11, c4 2.72 vs 1.84,
+      // c2 bf16 0.49 vs 0.36, c2 0.84 vs 0.64): four times the record loads
+      // and address work per gathered byte)
       // (measured at c2 fp32: one warp per token with 6 chunks and 2 CTAs/SM
       // beats 2-3 warps per token at 3-4 CTAs/SM, 0.641 vs 0.698-0.942 ms;
       // L2 evict_last/evict_first splits of the table stack: 0.68-0.81 ms)

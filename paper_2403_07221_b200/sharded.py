@@ -128,6 +128,10 @@ class ShardedLookupFFN:
         n = x.shape[0]
         if self.hash_mode == "token":
             codes, coeff = self.exchange_records(x)
+            if self.combine == "reduce_scatter":
+                # records in chunk order (chunk c of every rank's row block
+                # contiguous): one gather launch fills a chunk's buffer
+                return self._table_reduce_scatter_records(x, out, codes, coeff)
             part = _RowGather(self.gather_fn, codes, coeff)
         else:
             part = _PartialFromX(self.partial_fn)
@@ -196,6 +200,37 @@ class ShardedLookupFFN:
             for r in range(P):
                 rows = slice(r * per_rank + c * sub, r * per_rank + (c + 1) * sub)
                 part(x[rows], buf[r * sub:(r + 1) * sub], rows)
+            works.append(dist.reduce_scatter_tensor(y[c * sub:(c + 1) * sub], buf,
+                                                    op=dist.ReduceOp.SUM, group=self.group,
+                                                    async_op=True))
+        for w in works:
+            w.wait()
+        return y
+
+    def _table_reduce_scatter_records(self, x, out, codes, coeff):
+        """Reduce-scatter from exchanged records: the records are permuted
+        once so that chunk c of every rank's token block is one contiguous
+        range, and each chunk is ONE gather launch into the staging buffer
+        of its collective (instead of P launches of n / (P C) tokens)."""
+        n, d = x.shape[0], self.cfg.d_out
+        P, C = self.world, self.chunks
+        if n % (P * C) != 0:
+            raise ValueError(f"reduce_scatter forward: n={n} must be a multiple of "
+                             f"world*chunks={P * C} (pad the batch)")
+        per_rank = n // P
+        sub = per_rank // C
+        hl = codes.shape[1]
+        pc = codes.view(P, C, sub, hl).transpose(0, 1).reshape(n, hl)
+        pw = coeff.view(P, C, sub, hl).transpose(0, 1).reshape(n, hl)
+        y = out if out is not None else x.new_empty((per_rank, d))
+        bufs = [x.new_empty((P * sub, d)) for _ in range(min(C, 2))]
+        works = []
+        for c in range(C):
+            buf = bufs[c % len(bufs)]
+            if len(works) >= len(bufs):
+                works[-len(bufs)].wait()  # buffer reuse after its collective
+            rows = slice(c * P * sub, (c + 1) * P * sub)
+            self.gather_fn(pc[rows], pw[rows], buf)
             works.append(dist.reduce_scatter_tensor(y[c * sub:(c + 1) * sub], buf,
                                                     op=dist.ReduceOp.SUM, group=self.group,
                                                     async_op=True))
