@@ -290,7 +290,7 @@ int launch_dense_tcgen05(int tau, int split, dim3 grid, size_t smem, cudaStream_
 }
 
 int make_tma_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
-                 uint32_t box_inner, uint32_t box_outer, bool bf16 = false) {
+                 uint32_t box_inner, uint32_t box_outer, bool bf16 = false, bool swizzle = true) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -309,7 +309,8 @@ int make_tma_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t ou
   const CUresult r = encode(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                             2, const_cast<void*>(base), dims, strides, box, estr,
                             CU_TENSOR_MAP_INTERLEAVE_NONE,
-                            box_inner * eb == 64   ? CU_TENSOR_MAP_SWIZZLE_64B
+                            !swizzle               ? CU_TENSOR_MAP_SWIZZLE_NONE
+                            : box_inner * eb == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
                             : box_inner * eb == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
                                                    : CU_TENSOR_MAP_SWIZZLE_128B,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -671,6 +672,10 @@ int launch_gather_group(lffn_ctx* c, const uint32_t* codes, const float* coeff, 
         LFFN_CUDA(cudaGetLastError());
         return LFFN_OK;
       }
+      // (K3s, table tiles staged in shared memory for 1024 tokens x 32
+      // columns -- tools/experiments/staged_gather.cuh -- measured slower:
+      // c2 1.06-1.18 ms with cp.async and a CTA barrier per table, 0.759 ms
+      // with TMA tiles and producer / consumer mbarriers, vs 0.641 ms)
       // (a narrow part-major walk -- one 16-byte chunk per lane, so a round
       // of resident warps touches 1/nchunks of every row and c3's 268 MB
       // stack fits L2 per part -- measured slower everywhere, with 8 tables
