@@ -17,6 +17,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include "checked.cuh"
+
 namespace lffn_gpu {
 
 struct GatherParams {
@@ -112,6 +114,7 @@ __global__ void __launch_bounds__(256) gather_direct_kernel(GatherParams p) {
       for (int v = 0; v < VEC; ++v) vals[t][v] = 0.f;
       if (t < ntok) {
         const uint32_t code = __ldg(cbase + (int64_t)t * p.ld + k);
+        LFFN_DCHECK(code < (uint32_t)p.rows);
         w[t] = __ldg(wbase + (int64_t)t * p.ld + k);
         if (colok) RowLoad<TT, VEC>::load(T + rec_table(p, k) * table_stride + (int64_t)code * p.d_out + col, vals[t]);
       }
@@ -170,6 +173,7 @@ __global__ void __launch_bounds__(256) gather_row_kernel(GatherParams p, int war
     for (int v = 0; v < VEC; ++v) acc[c][v] = 0.f;
 
   auto row_loads = [&](int k, uint32_t code, float (&vals)[MAXC][VEC]) {
+    LFFN_DCHECK(code < (uint32_t)p.rows && k < p.nk);
     const TT* rp = T + k * tstride + (int64_t)code * p.d_out + colbase;
 #pragma unroll
     for (int c = 0; c < MAXC; ++c) {
@@ -396,6 +400,7 @@ __global__ void __launch_bounds__(256, MINB) gather_row_persistent_kernel(Gather
         uint4 raw[TIF][MAXC];
 #pragma unroll
         for (int q = 0; q < TIF; ++q) {
+          LFFN_DCHECK(codesG[q0 + q] < (uint32_t)p.rows && kg + q0 + q < p.nk && kg + q0 + q >= 0);
           const TT* rp = T + (kg + q0 + q) * tstride + (int64_t)codesG[q0 + q] * p.d_out + colbase;
 #pragma unroll
           for (int c = 0; c < MAXC; ++c)
@@ -505,6 +510,7 @@ __global__ void __launch_bounds__(256, 2) gather_split_kernel(GatherParams p, in
         uint4 raw[TIF][MAXC];
 #pragma unroll
         for (int q = 0; q < TIF; ++q) {
+          LFFN_DCHECK(code4[q0 + q] < (uint32_t)p.rows && kb + it + q0 + q < p.nk);
           const TT* rp = T + (int64_t)(kb + it + q0 + q) * tstride + (int64_t)code4[q0 + q] * p.d_out + colbase;
 #pragma unroll
           for (int c = 0; c < MAXC; ++c)

@@ -29,6 +29,7 @@
 #include <string>
 
 #include "lffn_gpu.h"
+#include "checked.cuh"
 #include "lffn_internal.h"
 
 using lffn_gpu::fail;
@@ -117,6 +118,7 @@ __global__ void pack_records_kernel(const uint32_t* __restrict__ codes, const fl
     const int kq0 = q * base + min(q, extra);
     const int hq = base + (q < extra ? 1 : 0);
     const int64_t dst = m * kq0 + i * hq + (k - kq0);
+    LFFN_DCHECK(dst >= 0 && dst < total && k - kq0 < hq);
     scodes[dst] = codes[e];
     scoeff[dst] = coeff[e];
   }

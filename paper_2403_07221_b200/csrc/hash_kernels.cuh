@@ -28,6 +28,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "checked.cuh"
+
 namespace lffn_gpu {
 
 struct HashParams {
@@ -357,6 +359,7 @@ __global__ void __launch_bounds__(NT, MINB) hash_structured_kernel(HashParams p)
           if (az < 18.5) w = __ddiv_rn(w, one_plus_exp_m2(az));
         }
       }
+      LFFN_DCHECK(k - p.kb < hl && base + tau <= p.code_width);
       p.codes[token * hl + (k - p.kb)] = code;
       p.coeff[token * hl + (k - p.kb)] = (float)(p.scaled ? __dmul_rn(w, sum_abs) : w);
     }

@@ -45,6 +45,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "checked.cuh"
 #include "hash_kernels.cuh"
 
 namespace lffn_gpu {
@@ -102,6 +103,7 @@ __device__ __forceinline__ void sf_flip(double (&v)[64], unsigned long long m) {
 // A layout <-> shared memory (thread t: indices 64 t + r; 128-bit accesses)
 template <int LOGD, bool STORE>
 __device__ __forceinline__ void sf_io_A(double* sm, double (&v)[64], int t) {
+  LFFN_DCHECK(SfGeom<LOGD>::pos(64 * t + 63) < SfGeom<LOGD>::PAD);
   double* q = sm + SfGeom<LOGD>::pos(64 * t);
 #pragma unroll
   for (int r = 0; r < 64; r += 2) {
@@ -118,6 +120,7 @@ __device__ __forceinline__ void sf_io_B(double* sm, double (&v)[64], int t) {
   using Gm = SfGeom<LOGD>;
 #pragma unroll
   for (int r = 0; r < 64; ++r) {
+    LFFN_DCHECK(Gm::pos(t + Gm::TPT * r) < Gm::PAD);
     double* q = sm + Gm::pos(t + Gm::TPT * r);
     if constexpr (STORE) *q = v[r];
     else v[r] = *q;
@@ -244,6 +247,7 @@ __global__ void __launch_bounds__(128, 3) hash_sf_kernel(HashSfParams p) {
   for (int k = p.kb + t; k < p.ke; k += TPT) {
     const int o = k * tau;
     const int wi = o >> 5, sh = o & 31;
+    LFFN_DCHECK(wi < Gm::WORDS && o + tau <= p.code_width);
     const uint32_t w_lo = words[wi];
     const uint32_t w_hi = (wi + 1 < Gm::WORDS) ? words[wi + 1] : 0u;
     const uint32_t code = __funnelshift_r(w_lo, w_hi, sh) & cmask;

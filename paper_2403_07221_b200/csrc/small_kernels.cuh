@@ -28,6 +28,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include "checked.cuh"
 #include "gather_kernels.cuh"
 #include "hash_kernels.cuh"
 
@@ -182,6 +183,7 @@ __global__ void __launch_bounds__(kSmallThreads) forward_small_kernel(SmallParam
   const double* z = buf[1];
   for (int j = tid; j < nk; j += kSmallThreads) {
     const int base = (k0 + j) * p.tau;
+    LFFN_DCHECK(j < kSmallMaxTpg && small_pos(base + p.tau - 1) < kSmallPad);
     uint32_t code = 0;
     double w = 1.0, sum_abs = 0.0;
     for (int q = 0; q < p.tau; ++q) {
@@ -215,6 +217,7 @@ __global__ void __launch_bounds__(kSmallThreads) forward_small_kernel(SmallParam
     uint4 raw[RB][MAXCH];
 #pragma unroll
     for (int q = 0; q < RB; ++q) {
+      LFFN_DCHECK(s_code[j + q] < (uint32_t)p.rows);
       const TT* rp = T + (int64_t)(kl0 + j + q) * tstride + (int64_t)s_code[j + q] * p.d_out;
 #pragma unroll
       for (int c = 0; c < MAXCH; ++c) {

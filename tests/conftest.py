@@ -34,6 +34,13 @@ def _ensure_built():
 
 _ensure_built()
 
+if os.environ.get("LFFN_TEST_CHECKED"):
+    # run the suite against the bounds-checked build (device asserts on
+    # data-derived indices; compute-sanitizer is closed on the GPU pool)
+    from paper_2403_07221_b200 import _capi as _c
+
+    _c.LIB_PATH = os.path.join(ROOT, "paper_2403_07221_b200", "csrc", "liblffn_gpu_checked.so")
+
 
 @pytest.fixture(scope="session")
 def oracle():
