@@ -577,3 +577,18 @@ def test_small_batch_host_graph_pinned():
         layer.forward_host_ptr(hx.data_ptr(), 8, hy.data_ptr())
     hx[0, 3] = 0.0
     layer.forward_host_ptr(hx.data_ptr(), 8, hy.data_ptr())
+
+
+def test_checked_build_is_the_one_loaded():
+    """LFFN_TEST_CHECKED=1 runs this suite against liblffn_gpu_checked.so
+    (device bounds asserts): prove that library is the one in the process."""
+    import os
+
+    from paper_2403_07221_b200 import _capi
+
+    _capi.lib()
+    maps = open("/proc/self/maps").read()
+    if os.environ.get("LFFN_TEST_CHECKED"):
+        assert "liblffn_gpu_checked.so" in maps and "csrc/liblffn_gpu.so" not in maps
+    else:
+        assert "csrc/liblffn_gpu.so" in maps
