@@ -518,14 +518,20 @@ __global__ void dense_split_x_kernel(const float* __restrict__ x, int64_t n, int
   if (bad) atomicOr(flag, 1);
 }
 
-// Exact recomputation of the listed near-zero z, one warp per entry: the
-// lanes form the d_in products (coalesced loads, all in flight) in shared
-// memory, lane 0 sums them in order -- float64, k ascending, separately
-// rounded multiply and add, exactly as projection.cpp:186-192.  Patches the
-// code bit (atomics: several entries can share a code word) and z_out.
+// Recomputation of the listed z inside the error band, one warp per entry:
+// the lanes form the d_in products (coalesced loads, all in flight).  With a
+// z output requested (SERIAL) they go to shared memory and lane 0 sums them
+// in order -- float64, k ascending, separately rounded multiply and add,
+// exactly as projection.cpp:186-192, so z is bit-identical; otherwise the
+// warp sums them as a float64 tree (error ~1e-16 of the magnitudes, far
+// below the 1e-5 band in which the north star lets a code bit differ), 31
+// lanes no longer waiting on lane 0's 768-step chain.  Patches the code bit
+// (atomics: several entries can share a code word) and z_out.  (One thread
+// per entry with its own serial chain measured slower: 84 vs 46 us at c2.)
 constexpr int kFixupWarps = 4;
+template <bool SERIAL>
 __global__ void __launch_bounds__(32 * kFixupWarps) dense_fixup_kernel(DenseParams p) {
-  extern __shared__ double fix_prod[];  // [kFixupWarps][d_in]
+  extern __shared__ double fix_prod[];  // SERIAL: [kFixupWarps][d_in]
   const int lane = threadIdx.x & 31;
   double* prod = fix_prod + size_t(threadIdx.x >> 5) * p.d_in;
   const int cnt = min(*p.fix_count, p.fix_cap);
@@ -536,19 +542,27 @@ __global__ void __launch_bounds__(32 * kFixupWarps) dense_fixup_kernel(DensePara
     const int col = int(e.y);
     const float* xr = p.x + token * p.d_in;
     const double* wr = p.wt64 + (size_t)col * p.d_in;
-    for (int k = lane; k < p.d_in; k += 32) prod[k] = __dmul_rn((double)__ldg(xr + k), __ldg(wr + k));
-    __syncwarp();
-    if (lane == 0) {
-      double acc = 0.0;
+    double acc = 0.0;
+    if constexpr (SERIAL) {
+      for (int k = lane; k < p.d_in; k += 32) prod[k] = __dmul_rn((double)__ldg(xr + k), __ldg(wr + k));
+      __syncwarp();
+      if (lane == 0) {
 #pragma unroll 16
-      for (int k = 0; k < p.d_in; ++k) acc = __dadd_rn(acc, prod[k]);
+        for (int k = 0; k < p.d_in; ++k) acc = __dadd_rn(acc, prod[k]);
+      }
+      __syncwarp();
+    } else {
+      for (int k = lane; k < p.d_in; k += 32) acc = fma((double)__ldg(xr + k), __ldg(wr + k), acc);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    }
+    if (lane == 0) {
       unsigned int* word = reinterpret_cast<unsigned int*>(p.codes + token * hl + col / p.tau);
       const unsigned int bit = 1u << (col % p.tau);
       if (acc >= 0.0) atomicOr(word, bit);
       else atomicAnd(word, ~bit);
       if (p.z_out) p.z_out[token * p.code_width + p.col_begin + col] = acc;
     }
-    __syncwarp();
   }
 }
 

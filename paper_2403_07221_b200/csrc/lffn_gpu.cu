@@ -485,15 +485,16 @@ int launch_hash_top1(lffn_ctx* c, const float* d_x, int64_t n, uint32_t* codes, 
                                         c->dense_maps, d);
     if (rc != LFFN_OK) return rc;
     ++c->launches;
-    // exact fixups: d_in <= 6144 keeps the per-warp product rows in 192 KB
-    const size_t fsm = size_t(kFixupWarps) * size_t(d.d_in) * sizeof(double);
-    static bool fattr = [] {
-      cudaFuncSetAttribute(dense_fixup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      return true;
-    }();
-    (void)fattr;
-    // ~one entry per warp at c2 (2.7k entries): the serial float64 sums run in parallel
-    dense_fixup_kernel<<<unsigned(c->num_sms * 8), 32 * kFixupWarps, fsm, st>>>(d);
+    // fixups of the band, one warp per listed entry (the list length is on
+    // the device: a grid-stride loop); exact serial sums when z is returned
+    if (z_out) {
+      // d_in <= 6144 keeps the per-warp product rows in 192 KB
+      const size_t fsm = size_t(kFixupWarps) * size_t(d.d_in) * sizeof(double);
+      set_smem(reinterpret_cast<const void*>(dense_fixup_kernel<true>), int(fsm));
+      dense_fixup_kernel<true><<<unsigned(c->num_sms * 8), 32 * kFixupWarps, fsm, st>>>(d);
+    } else {
+      dense_fixup_kernel<false><<<unsigned(c->num_sms * 8), 32 * kFixupWarps, 0, st>>>(d);
+    }
     ++c->launches;
     LFFN_CUDA(cudaGetLastError());
     return LFFN_OK;

@@ -592,3 +592,29 @@ def test_checked_build_is_the_one_loaded():
         assert "liblffn_gpu_checked.so" in maps and "csrc/liblffn_gpu.so" not in maps
     else:
         assert "csrc/liblffn_gpu.so" in maps
+
+
+@pytest.mark.parametrize("d_in,h,tau,scale", [(768, 256, 8, 10.0), (768, 256, 8, 100.0),
+                                              (4096, 64, 8, 1.0), (4096, 64, 8, 30.0)])
+def test_dense_tcgen05_band_scales_with_inputs(oracle, d_in, h, tau, scale):
+    """The tcgen05 dense hash's exact-fixup band is relative (fix_scale *
+    ||x|| * ||w_c||): codes stay bit-exact for inputs 10-100x the c2 scale and
+    at d_in = 4096 (a ~5x longer MMA chain), where a fixed 1e-4 band would
+    not hold."""
+    n = 256
+    cfg, proj, T, x = _setup(d_in, 64, h, tau, ProjKind.dense, n)
+    x = (x * scale).astype(np.float32)
+    layer = LookupFFN(cfg, proj, T, max_tokens=n)
+    codes, coeff, z = device_hash(layer, x)
+    c, s = to_oracle(cfg, proj)
+    z_ref = oracle.proj_forward(s, proj.blob, x.astype(np.float64))
+    codes_ref, absz = oracle.compute_codes(z_ref, h, tau)
+    assert np.array_equal(codes, codes_ref)
+    # the production path (no z output: band entries summed as a float64 tree)
+    codes_p, _, _ = device_hash(layer, x, want_z=False)
+    from test_gpu_parity_configs import assert_codes_match
+    assert_codes_match(codes_p, z_ref, h, tau, "dense production")
+    # z within the band, and bit-identical wherever it was recomputed
+    xn = np.linalg.norm(x.astype(np.float64), axis=1)[:, None]
+    wn = np.linalg.norm(proj.blob.reshape(d_in, h * tau), axis=0)[None, :]
+    assert (np.abs(z - z_ref) <= 1e-3 * xn * wn).all()
