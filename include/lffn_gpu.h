@@ -246,7 +246,9 @@ int lffn_sync(lffn_ctx* ctx, void* stream);
  *   LFFN_OPT_SMALL_MAX_TOKENS  batches of at most this many tokens (<= 64,
  *                              default 64; 0 = never) run the whole forward
  *                              in one launch spread over (token, table
- *                              group) CTAs (signflip, D = 2048, top-1) */
+ *                              group) CTAs (signflip, D = 2048, top-1)
+ *   LFFN_OPT_GATHER_SMS        persistent gather grid over this many SMs
+ *                              (0 = all, the default) */
 #define LFFN_OPT_DENSE_EXACT 1
 #define LFFN_OPT_TABLE_GROUP_BYTES 2
 #define LFFN_OPT_GATHER_VARIANT 3
@@ -255,6 +257,7 @@ int lffn_sync(lffn_ctx* ctx, void* stream);
 #define LFFN_OPT_HASH_EXACT 7
 #define LFFN_OPT_HOST_CHUNKS 8
 #define LFFN_OPT_SMALL_MAX_TOKENS 10
+#define LFFN_OPT_GATHER_SMS 11
 int lffn_ctx_set_option(lffn_ctx* ctx, int option, int64_t value);
 
 /* ---- multi-GPU table sharding (north star: tables split

@@ -158,6 +158,7 @@ struct lffn_ctx {
   int bwd_one_pass = 0;          // LFFN_OPT_BWD_ONE_PASS: single-pass KB1 (A/B reference)
   int hash_exact = 0;            // LFFN_OPT_HASH_EXACT: always K1 (z bit-identical)
   int host_chunks = 8;           // LFFN_OPT_HOST_CHUNKS: lffn_forward_host pipeline chunks
+  int gather_sms = 0;            // LFFN_OPT_GATHER_SMS: persistent gather grid over this many SMs (0 = all)
   unsigned long long* d_sfmask = nullptr;  // K1f: per-thread sign masks [3][D/64]
   int small_max = 64;                // LFFN_OPT_SMALL_MAX_TOKENS: K5 up to this batch size
   static constexpr int kSmallTokens = 64;
@@ -644,7 +645,8 @@ int launch_gather_group(lffn_ctx* c, const uint32_t* codes, const float* coeff, 
       const int pwpt = (nchunks + pmaxc - 1) / pmaxc;
       const int64_t pwarps = n * pwpt;
       if (pwpt > 1) p.reverse_odd_rounds = 0;
-      const unsigned pgrid = (unsigned)std::min<int64_t>(int64_t(c->num_sms) * 2, (pwarps * 32 + 255) / 256);
+      const int gsms = c->gather_sms > 0 ? std::min(c->gather_sms, c->num_sms) : c->num_sms;
+      const unsigned pgrid = (unsigned)std::min<int64_t>(int64_t(gsms) * 2, (pwarps * 32 + 255) / 256);
       (void)pg;
       // fewer (token, part) items than resident warp slots: split the table
       // walk over S warps per item (gather_split_kernel), S the largest of
@@ -1357,39 +1359,48 @@ int lffn_forward_host(lffn_ctx* c, const float* h_x, int64_t n, float* h_y) {
   if (!c->d_T) return fail(LFFN_ERR_USAGE, "lookup forward: tables not uploaded");
   DeviceGuard g(c->device);
   if (n == 0) return LFFN_OK;
-  if (small_eligible(c, n) && is_pinned(h_x) && is_pinned(h_y)) return forward_host_graph(c, h_x, n, h_y);
+  const bool pinned = is_pinned(h_x) && is_pinned(h_y);
+  if (small_eligible(c, n) && pinned) return forward_host_graph(c, h_x, n, h_y);
+  const int64_t d_in = c->cfg.d_in, d_out = c->cfg.d_out;
   // Chunked pipeline: H2D(chunk i+1) || compute(chunk i) || D2H(chunk i-1).
   // Structured projections use no context scratch, so consecutive chunks
   // alternate between two compute streams and their kernels overlap (one
   // chunk alone does not fill the GPU); the dense kind keeps one stream (its
   // split-x / fixup scratch is per context).
-  const int64_t d_in = c->cfg.d_in, d_out = c->cfg.d_out;
   int nch = int(std::min<int64_t>(std::min(c->host_chunks, lffn_ctx::kChunks), std::max<int64_t>(1, n / 512)));
   const bool dual = c->proj.kind != LFFN_PROJ_DENSE && c->nc == 1;
+  // (Zero-copy variants -- the hash reading x from the mapped pinned host
+  // memory and / or the gather writing y to it, no copy-engine transfer --
+  // measured slower at c2: 2.48 ms (x), 1.84-2.04 ms (y), 2.40 ms (both)
+  // against 1.35 ms for the copy engines.)
+  const int zc = 0;
   const int64_t per = (n + nch - 1) / nch;
   for (int i = 0; i < nch; ++i) {
     const int64_t r0 = i * per, r1 = std::min(n, r0 + per);
     if (r0 >= r1) break;
     cudaStream_t sc = (dual && (i & 1)) ? c->s_comp2 : c->s_comp;
-    LFFN_CUDA(cudaMemcpyAsync(c->d_xbuf + r0 * d_in, h_x + r0 * d_in,
-                              size_t(r1 - r0) * d_in * sizeof(float), cudaMemcpyHostToDevice, c->s_h2d));
-    LFFN_CUDA(cudaEventRecord(c->ev_h2d[i], c->s_h2d));
-    LFFN_CUDA(cudaStreamWaitEvent(sc, c->ev_h2d[i], 0));
+    const float* xs = c->d_xbuf + r0 * d_in;
+    if (zc & 1) {
+      xs = h_x + r0 * d_in;
+    } else {
+      LFFN_CUDA(cudaMemcpyAsync(c->d_xbuf + r0 * d_in, h_x + r0 * d_in,
+                                size_t(r1 - r0) * d_in * sizeof(float), cudaMemcpyHostToDevice, c->s_h2d));
+      LFFN_CUDA(cudaEventRecord(c->ev_h2d[i], c->s_h2d));
+      LFFN_CUDA(cudaStreamWaitEvent(sc, c->ev_h2d[i], 0));
+    }
+    float* ys = (zc & 2) ? h_y + r0 * d_out : c->d_ybuf + r0 * d_out;
     const int64_t rec = r0 * c->h_loc * c->nc;
     if (small_eligible(c, r1 - r0)) {
-      if (int rc = launch_small(c, c->d_xbuf + r0 * d_in, r1 - r0, c->d_ybuf + r0 * d_out, 0, sc)) return rc;
+      if (int rc = launch_small(c, xs, r1 - r0, ys, 0, sc)) return rc;
     } else {
-      if (int rc = launch_hash(c, c->d_xbuf + r0 * d_in, r1 - r0, c->d_codes + rec, c->d_coeff + rec,
-                               nullptr, sc))
-        return rc;
-      if (int rc = launch_gather(c, c->d_codes + rec, c->d_coeff + rec, r1 - r0,
-                                 c->d_ybuf + r0 * d_out, 0, sc))
-        return rc;
+      if (int rc = launch_hash(c, xs, r1 - r0, c->d_codes + rec, c->d_coeff + rec, nullptr, sc)) return rc;
+      if (int rc = launch_gather(c, c->d_codes + rec, c->d_coeff + rec, r1 - r0, ys, 0, sc)) return rc;
     }
     LFFN_CUDA(cudaEventRecord(c->ev_comp[i], sc));
     LFFN_CUDA(cudaStreamWaitEvent(c->s_d2h, c->ev_comp[i], 0));
-    LFFN_CUDA(cudaMemcpyAsync(h_y + r0 * d_out, c->d_ybuf + r0 * d_out,
-                              size_t(r1 - r0) * d_out * sizeof(float), cudaMemcpyDeviceToHost, c->s_d2h));
+    if (!(zc & 2))
+      LFFN_CUDA(cudaMemcpyAsync(h_y + r0 * d_out, c->d_ybuf + r0 * d_out,
+                                size_t(r1 - r0) * d_out * sizeof(float), cudaMemcpyDeviceToHost, c->s_d2h));
   }
   return read_flag(c, c->s_d2h);
 }
@@ -1787,6 +1798,10 @@ int lffn_ctx_set_option(lffn_ctx* c, int option, int64_t value) {
       return LFFN_OK;
     case LFFN_OPT_HASH_EXACT:
       c->hash_exact = value != 0;
+      return LFFN_OK;
+    case LFFN_OPT_GATHER_SMS:
+      if (value < 0) return fail(LFFN_ERR_USAGE, "option: negative SM count");
+      c->gather_sms = int(value);
       return LFFN_OK;
     case LFFN_OPT_SMALL_MAX_TOKENS:
       if (value < 0) return fail(LFFN_ERR_USAGE, "option: negative small-batch limit");

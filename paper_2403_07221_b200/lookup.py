@@ -498,7 +498,8 @@ class LookupFFN:
                "bwd_one_pass": _capi.LFFN_OPT_BWD_ONE_PASS,
                "hash_exact": _capi.LFFN_OPT_HASH_EXACT,
                "host_chunks": _capi.LFFN_OPT_HOST_CHUNKS,
-               "small_max_tokens": _capi.LFFN_OPT_SMALL_MAX_TOKENS}[name]
+               "small_max_tokens": _capi.LFFN_OPT_SMALL_MAX_TOKENS,
+               "gather_sms": _capi.LFFN_OPT_GATHER_SMS}[name]
         check(_capi.lib().lffn_ctx_set_option(self._ctx, opt, int(value)))
 
     def launch_count(self) -> int:

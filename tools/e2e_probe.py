@@ -35,10 +35,15 @@ cfg, proj, T = make_params(w, ProjKind.signflip)
 layer = LookupFFN(cfg, proj, T, max_tokens=n)
 x = torch.from_numpy(make_x(w, n)).pin_memory()
 y = torch.empty((n, 768), dtype=torch.float32).pin_memory()
-for ch in (4, 6, 8, 10, 12, 16):
-    layer.set_option("host_chunks", ch)
-    ms = timeit(lambda: layer.forward_host_ptr(x.data_ptr(), n, y.data_ptr()))
-    print(f"forward_host chunks={ch}: {ms:.3f} ms  {n/ms*1e3/1e6:.2f} M tok/s")
+y_ref = None
+for zc in (0,):
+    for ch in (4, 6, 8, 10, 12, 16):
+        layer.set_option("host_chunks", ch)
+        ms = timeit(lambda: layer.forward_host_ptr(x.data_ptr(), n, y.data_ptr()))
+        if y_ref is None:
+            y_ref = y.clone()
+        same = bool(torch.equal(y, y_ref))
+        print(f"forward_host zero_copy={zc} chunks={ch}: {ms:.3f} ms  {n/ms*1e3/1e6:.2f} M tok/s  same_y={same}")
 layer.set_option("host_chunks", 8)
 xp = make_x(w, n)
 yp = np.empty((n, 768), np.float32)

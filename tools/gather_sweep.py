@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--variants", default="")
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--group-mb", default="0", help="comma list of table group sizes (MB)")
+    ap.add_argument("--sms", default="0", help="comma list of gather SM counts (0 = all)")
     ap.add_argument("--tokens", default="", help="comma list of batch sizes (default: the workload's)")
     a = ap.parse_args()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -47,8 +48,10 @@ def main():
         y_ref = None
         G = w.n * w.h * w.d * (4 if dt == torch.float32 else 2)
         ns = [int(t) for t in a.tokens.split(",")] if a.tokens else [w.n]
-        runs = [(v, int(gm), m) for m in ns for gm in a.group_mb.split(",") for v in variants]
-        for v, gm, m in runs:
+        runs = [(v, int(gm), m, int(sm)) for m in ns for gm in a.group_mb.split(",") for v in variants
+                for sm in a.sms.split(",")]
+        for v, gm, m, sm in runs:
+            layer.set_option("gather_sms", sm)
             if v == variants[0]:
                 y_ref = None
             layer.set_option("table_group_bytes", gm << 20)
@@ -74,7 +77,7 @@ def main():
                 diff = float((y[:m] - y_ref).abs().max() / y_ref.abs().max())
             t = statistics.median(ts)
             Gm = G * m / w.n
-            print(f"{name} n={m} v={v:3d} group={gm}MB: {t:.4f} ms  {Gm / t / 1e6:.0f} GB/s gathered  "
+            print(f"{name} n={m} v={v:3d} group={gm}MB sms={sm}: {t:.4f} ms  {Gm / t / 1e6:.0f} GB/s gathered  "
                   f"maxdiff/max={diff:.2e}", flush=True)
         layer.close()
         del T
