@@ -20,26 +20,40 @@
 // backward's recompute) the launcher takes K1 (hash_kernels.cuh) instead.
 //
 // Layout: TPT = D / 64 threads own one token, 64 float64 registers each.
-//   A: thread t holds indices 64 t + r            (index bits 0-5 in registers)
-//   B: thread t holds indices t + TPT r          (bits log2(TPT) .. +5 in registers)
+//   B: thread t, register q holds index t + TPT q    (the high index bits in registers)
+//   A: thread t, register q holds index 64 t + pi(q) (64 consecutive indices;
+//      pi(q) = 32 (q & 1) + (q >> 1) for D = 2048, pi(q) = q for D = 4096)
 // Every transform runs the same code: sign flip, butterflies over the six
-// index bits in the registers, one transpose through shared memory (64-bit
-// stores in the B pattern, 128-bit loads in the A pattern; both bank-conflict
-// free with two padding doubles per 64), butterflies over the bits the
-// transpose brought into the registers.  The stages of a Walsh-Hadamard
-// transform commute, so which bits sit in the registers may differ from
-// transform to transform: x starts in a layout L0 chosen so that three
-// transposes end in layout A (sf_start_index).  Three transposes per token
-// against K1's six stores and five loads.
+// register bits, one transpose through shared memory (64-bit stores at
+// position t + TPT q, 128-bit loads of positions 64 t + pi(q); both
+// bank-conflict free with two padding doubles per 64), butterflies over the
+// register bits the transpose brought in (q bits 1-5 for D = 2048, where
+// register bit 0 -- index bit 5 -- stays in the registers; all six for D =
+// 4096).  The transpose is an involution on (thread, register), so the
+// layouts alternate B, A, B, A: x is loaded in layout B (coalesced: lane t
+// reads x[t + TPT q]) and the third transform ends in layout A.
+//
+// Zero padding: in layout B the padded coordinates (index >= d_in) are whole
+// registers q >= ceil(d_in / TPT), the same in every thread.  The kernel is
+// instantiated per LIVE (live registers, a multiple of 8): the first
+// transform's first butterflies skip pairs of zeros and turn (x, 0) pairs
+// into copies (x + 0 and x - 0 are exact), the loads, conversions and sign
+// flips touch live registers only -- at c2 (d_in = 768 of 2048) 120 instead
+// of 384 float64 adds in that phase, at c3 (1024 of 2048) 160.
 //
 // Epilogue in layout A: a thread's 64 registers are 64 consecutive
 // coordinates, so its sign bits (z >= 0, lookup.cpp:77) form two words of the
 // h*tau code bits in shared memory, from which each thread funnel-shifts its
-// tables' codes.  The weight is exactly 1.0 for a table whose every |z_j| >= 18.5
-// (1 + exp(-2|z|) rounds to 1.0); the rare small coordinates (a second
-// ballot) have their z stored, and the table's weight divides by
-// 1 + exp(-2|z_j|) over exactly those j in ascending order -- the reference's
-// sequential division, the other factors being exact divisions by 1.0.
+// tables' codes.  The common case is integer-only: the sign bits of the high
+// words are funnelled into the two words, and an unsigned min / max over the
+// doubled high words (|z| without its sign) tells whether any coordinate is
+// small (|z| < 18.5, which includes the -0.0 whose sign bit must not count)
+// or non-finite.  Only then the float64 compares run.  The weight is exactly
+// 1.0 for a table whose every |z_j| >= 18.5 (1 + exp(-2|z|) rounds to 1.0);
+// the rare small coordinates have their z stored, and the table's weight
+// divides by 1 + exp(-2|z_j|) over exactly those j in ascending order -- the
+// reference's sequential division, the other factors being exact divisions
+// by 1.0.
 #pragma once
 
 #include <cstdint>
@@ -57,6 +71,7 @@ struct HashSfParams {
   int code_width;              // h * tau
   int tau;
   int kb, ke;                  // tables owned: [kb, ke)
+  int transforms;              // 3 (Projection::forward signflip: H S2 H S1 H S0)
   const unsigned long long* masks;  // [3][TPT]: bit r = sign of the element thread t holds in
                                // register r at the start of transform tr (sf_layout_index)
   uint32_t* codes;             // [n x (ke - kb)]
@@ -71,8 +86,16 @@ struct SfGeom {
   static constexpr int LOGT = LOGD - 6;
   static constexpr int PAD = D + 2 * (D >> 6);       // doubles per token in shared memory
   static constexpr int WORDS = D / 32;               // sign words per token
+  static constexpr int B2 = LOGD == 11 ? 1 : 0;      // first register bit of the second butterflies
   // shared-memory position of index a (two padding doubles per 64)
-  static __device__ __forceinline__ int pos(int a) { return a + 2 * (a >> 6); }
+  static __host__ __device__ __forceinline__ constexpr int pos(int a) { return a + 2 * (a >> 6); }
+  // layout A: register q of thread t holds index 64 t + pi(q); pinv inverts pi
+  static __host__ __device__ __forceinline__ constexpr int pi(int q) {
+    return LOGD == 11 ? 32 * (q & 1) + (q >> 1) : q;
+  }
+  static __host__ __device__ __forceinline__ constexpr int pinv(int r) {
+    return LOGD == 11 ? ((r & 31) << 1) | (r >> 5) : r;
+  }
 };
 
 // butterflies over register bits [B0, B1) in ascending order
@@ -91,70 +114,108 @@ __device__ __forceinline__ void sf_stages(double (&v)[64]) {
   }
 }
 
+// Registers known to be zero before stage k when registers q >= live start
+// as zeros and the stages run in ascending order: a (zero, zero) pair stays
+// zero, an (x, zero) pair becomes two copies of x.
+__host__ __device__ constexpr unsigned long long sf_zero_mask(int live, int k) {
+  unsigned long long z = live >= 64 ? 0ull : ~0ull << live;
+  for (int s = 0; s < k; ++s)
+    for (int r = 0; r < 64; ++r) {
+      if (r & (1 << s)) continue;
+      const int b = r | (1 << s);
+      const bool za = (z >> r) & 1ull, zb = (z >> b) & 1ull;
+      if (!(za && zb)) z &= ~((1ull << r) | (1ull << b));
+    }
+  return z;
+}
+
+template <int LIVE, int K>
+__device__ __forceinline__ void sf_stage_live(double (&v)[64]) {
+  constexpr unsigned long long Z = sf_zero_mask(LIVE, K);
+#pragma unroll
+  for (int r = 0; r < 64; ++r) {
+    if (r & (1 << K)) continue;
+    const int b = r | (1 << K);
+    const bool za = (Z >> r) & 1ull, zb = (Z >> b) & 1ull;
+    if (za && zb) continue;           // 0 + 0, 0 - 0
+    if (zb) { v[b] = v[r]; continue; }  // x + 0 = x - 0 = x
+    const double x = v[r], y = v[b];  // (a zero x with a live y cannot occur: the zeros are a suffix)
+    v[r] = __dadd_rn(x, y);
+    v[b] = __dsub_rn(x, y);
+  }
+}
+
+// the six register stages of the first transform, registers q >= LIVE zero
+template <int LIVE>
+__device__ __forceinline__ void sf_stages_live(double (&v)[64]) {
+  if constexpr (LIVE >= 64) {
+    sf_stages<0, 6>(v);
+  } else {
+    sf_stage_live<LIVE, 0>(v);
+    sf_stage_live<LIVE, 1>(v);
+    sf_stage_live<LIVE, 2>(v);
+    sf_stage_live<LIVE, 3>(v);
+    sf_stage_live<LIVE, 4>(v);
+    sf_stage_live<LIVE, 5>(v);
+  }
+}
+
+template <int NQ>
 __device__ __forceinline__ void sf_flip(double (&v)[64], unsigned long long m) {
   const uint32_t lo = (uint32_t)m, hi = (uint32_t)(m >> 32);
 #pragma unroll
-  for (int r = 0; r < 64; ++r) {
+  for (int r = 0; r < NQ; ++r) {
     const uint32_t bit = ((r < 32 ? lo : hi) >> (r & 31)) & 1u;
     v[r] = __hiloint2double(__double2hiint(v[r]) ^ (int)(bit << 31), __double2loint(v[r]));
   }
 }
 
-// A layout <-> shared memory (thread t: indices 64 t + r; 128-bit accesses)
-template <int LOGD, bool STORE>
-__device__ __forceinline__ void sf_io_A(double* sm, double (&v)[64], int t) {
-  LFFN_DCHECK(SfGeom<LOGD>::pos(64 * t + 63) < SfGeom<LOGD>::PAD);
-  double* q = sm + SfGeom<LOGD>::pos(64 * t);
+// layout A <- shared memory (thread t: positions 64 t + pi(q); 128-bit loads
+// of position pairs (2m, 2m + 1))
+template <int LOGD>
+__device__ __forceinline__ void sf_load_A(const double* sm, double (&v)[64], int t) {
+  using Gm = SfGeom<LOGD>;
+  LFFN_DCHECK(Gm::pos(64 * t + 63) < Gm::PAD);
+  const double* q = sm + Gm::pos(64 * t);
 #pragma unroll
   for (int r = 0; r < 64; r += 2) {
-    double2* d = reinterpret_cast<double2*>(q + r);
-    if constexpr (STORE) *d = make_double2(v[r], v[r + 1]);
-    else { const double2 w = *d; v[r] = w.x; v[r + 1] = w.y; }
+    const double2 w = *reinterpret_cast<const double2*>(q + r);
+    v[Gm::pinv(r)] = w.x;
+    v[Gm::pinv(r + 1)] = w.y;
   }
 }
 
-// B layout <-> shared memory (thread t: indices t + TPT r; 64-bit accesses,
+// layout B -> shared memory (thread t: positions t + TPT q; 64-bit stores,
 // consecutive across the threads of a warp)
-template <int LOGD, bool STORE>
-__device__ __forceinline__ void sf_io_B(double* sm, double (&v)[64], int t) {
+template <int LOGD>
+__device__ __forceinline__ void sf_store_B(double* sm, const double (&v)[64], int t) {
   using Gm = SfGeom<LOGD>;
 #pragma unroll
   for (int r = 0; r < 64; ++r) {
     LFFN_DCHECK(Gm::pos(t + Gm::TPT * r) < Gm::PAD);
-    double* q = sm + Gm::pos(t + Gm::TPT * r);
-    if constexpr (STORE) *q = v[r];
-    else v[r] = *q;
+    sm[Gm::pos(t + Gm::TPT * r)] = v[r];
   }
 }
 
-// Index held by thread t in register r at the start (layout L0).  The
-// transpose (store at index t + TPT r, load index 64 t' + r') maps layout L
-// to L'(t', r') = L(r' mod TPT, (TPT/32) t' ... ) -- for D = 4096 it swaps t
-// and r, for D = 2048 L'(l, r) = L(r & 31, 2 l + (r >> 5)).  L0 is chosen so
-// that three transposes end in layout A (index 64 t + r):
-//   D = 2048: L0 = 1024 (l & 1) + 32 (r >> 1) + 16 (r & 1) + (l >> 1)
-//             L1 = 32 l + 1024 (r & 1) + (r >> 1),  L2 = l + 32 r (= B),  L3 = A
-//   D = 4096: L0 = t + 64 r (= B), L1 = A, L2 = B, L3 = A
-// Each transform's first butterflies cover the six index bits its layout
-// holds in registers, the second ones the register bits that came from the
-// threads (D = 2048: register bits 0-4; D = 4096: all six), i.e. every bit
-// exactly once.  The host builds the sign masks in L0, L1, L2.
-template <int LOGD>
-__host__ __device__ __forceinline__ int sf_start_index(int t, int r) {
-  if constexpr (LOGD == 11) return 1024 * (t & 1) + 32 * (r >> 1) + 16 * (r & 1) + (t >> 1);
-  else return t + 64 * r;
-}
-__host__ __device__ __forceinline__ int sf_layout_index(int logd, int tr, int t, int r) {
-  if (logd == 12) return (tr & 1) ? 64 * t + r : t + 64 * r;
-  if (tr == 0) return sf_start_index<11>(t, r);
-  if (tr == 1) return 32 * t + 1024 * (r & 1) + (r >> 1);
-  if (tr == 2) return t + 32 * r;
-  return 64 * t + r;
+// Index held by thread t in register q at the start of transform tr (the
+// host builds the sign masks in these layouts): B, A, B.
+__host__ __device__ __forceinline__ int sf_layout_index(int logd, int tr, int t, int q) {
+  if (logd == 12) return (tr & 1) ? 64 * t + q : t + 64 * q;
+  return (tr & 1) ? 64 * t + SfGeom<11>::pi(q) : t + 32 * q;
 }
 
 __device__ __noinline__ double sf_one_plus_exp_m2(double a) { return __dadd_rn(1.0, exp(-2.0 * a)); }
 
-template <int LOGD>
+// live registers of layout B for an input width: ceil(d_in / TPT) rounded up
+// to the instantiated classes
+__host__ __device__ constexpr int sf_live_class(int logd, int d_in) {
+  const int tpt = (1 << logd) / 64;
+  const int need = (d_in + tpt - 1) / tpt;
+  if (logd == 12) return need <= 32 ? 32 : 64;
+  return need <= 16 ? 16 : need <= 24 ? 24 : need <= 32 ? 32 : need <= 48 ? 48 : 64;
+}
+
+template <int LOGD, int LIVE>
 __global__ void __launch_bounds__(128, 3) hash_sf_kernel(HashSfParams p) {
   using Gm = SfGeom<LOGD>;
   constexpr int TPT = Gm::TPT;
@@ -176,74 +237,127 @@ __global__ void __launch_bounds__(128, 3) hash_sf_kernel(HashSfParams p) {
   int bad = 0;
   double v[64];
 
-  // ---- x (padded to D) into the start layout L0 (below); the finiteness
-  // test rides on an FMA chain (x * 0 is NaN iff x is inf / NaN)
+  // ---- x (padded to D) into layout B: register q of thread t holds
+  // x[t + TPT q]; registers q >= LIVE are padding (launcher: d_in <= TPT *
+  // LIVE).  The finiteness test rides on an FMA chain (x * 0 is NaN iff x is
+  // inf / NaN).
   {
     const float* xr = p.x + token * (int64_t)p.d_in;
     float nanacc = 0.f;
+    constexpr int LB = LIVE <= 32 ? LIVE : LIVE / 2;  // loads in flight per thread
 #pragma unroll
-    for (int g = 0; g < 64; g += 16) {
-      float f[16];
+    for (int g = 0; g < LIVE; g += LB) {
+      float f[LB];
 #pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        const int a = sf_start_index<LOGD>(t, g + r);
+      for (int r = 0; r < LB; ++r) {
+        const int a = t + TPT * (g + r);
         f[r] = a < p.d_in ? __ldg(xr + a) : 0.f;
       }
 #pragma unroll
-      for (int r = 0; r < 16; ++r) {
+      for (int r = 0; r < LB; ++r) {
         nanacc = fmaf(f[r], 0.f, nanacc);
         v[g + r] = (double)f[r];
       }
     }
+#pragma unroll
+    for (int r = LIVE; r < 64; ++r) v[r] = 0.0;
     if (nanacc != nanacc) bad |= 1;
   }
-  // Three transforms with the same code: sign flip, butterflies over the six
-  // register bits, the transpose (store in the B pattern, load in the A
-  // pattern: it moves the value of thread / register (r' mod T, T' (...))
-  // -- see sf_start_index), butterflies over the register bits the
-  // transpose brought in from the threads.  The transpose permutes which
-  // index bits sit in the registers so that every transform covers each of
-  // its log2(D) bits exactly once, and three of them take the start layout
-  // L0 to layout A.  The loop is not unrolled: one copy of the butterfly code
-  // (the kernel stays within the 32 KB L1.5 instruction cache).
+  // Three transforms: sign flip, butterflies over the six register bits, the
+  // transpose, butterflies over the register bits it brought in.  The first
+  // transform's first half is specialised for the zero padding; everything
+  // after it is one copy of code in a loop that is not unrolled (the hot loop
+  // stays within the 32 KB L1.5 instruction cache).
+  sf_flip<LIVE>(v, __ldg(p.masks + t));
+  sf_stages_live<LIVE>(v);
+  sf_store_B<LOGD>(sm, v, t);  // (the copies of the padding pairs are stored straight from their source)
+  // (the trip count comes from the parameters so that the compiler keeps one
+  // copy of the body instead of peeling the first transform's second half)
 #pragma unroll 1
-  for (int tr = 0; tr < 3; ++tr) {
-    sf_flip(v, __ldg(p.masks + tr * TPT + t));
-    sf_stages<0, 6>(v);
-    sf_io_B<LOGD, true>(sm, v, t);
+  for (int tr = 1; tr <= p.transforms; ++tr) {
     token_sync();
-    sf_io_A<LOGD, false>(sm, v, t);
+    sf_load_A<LOGD>(sm, v, t);
     token_sync();
-    sf_stages<0, (LOGD == 11 ? 5 : 6)>(v);
+    sf_stages<Gm::B2, 6>(v);
+    if (tr < p.transforms) {
+      sf_flip<64>(v, __ldg(p.masks + tr * TPT + t));
+      sf_stages<0, 6>(v);
+      sf_store_B<LOGD>(sm, v, t);
+    }
   }
 
-  // ---- epilogue in layout A: z[64 t + r] = v[r]
+  // ---- epilogue in layout A: z[64 t + r] = v[pinv(r)]
   // sign bits (z >= 0, lookup.cpp:77), small-|z| bits (|z| < 18.5) and the
   // finiteness of the first h*tau outputs (projection.cpp:264, lookup.cpp:204)
   uint32_t s0 = 0, s1 = 0, m0 = 0, m1 = 0;
-  bool fin = true;
+  {
+    // integer pass: negative-sign words (four funnel chains) and, per group
+    // of eight coordinates, the range of |z|'s high words
+    constexpr uint32_t kSmallHi = 0x40328000u, kInfHi = 0x7ff00000u;
+    uint32_t n[4] = {0u, 0u, 0u, 0u};
+    uint32_t gsmall = 0u;  // bit g: group g (coordinates 8 g .. 8 g + 7) holds a small or non-finite value
 #pragma unroll
-  for (int r = 0; r < 64; ++r) {
-    const uint32_t sb = v[r] >= 0.0 ? 1u : 0u;
-    const uint32_t mb = fabs(v[r]) < 18.5 ? 1u : 0u;
-    if (r < 32) { s0 |= sb << r; m0 |= mb << r; }
-    else { s1 |= sb << (r - 32); m1 |= mb << (r - 32); }
-    if (64 * t + r < p.code_width) fin &= (__double2hiint(v[r]) & 0x7ff00000) != 0x7ff00000;
+    for (int g = 7; g >= 0; --g) {
+      uint32_t umin = 0xffffffffu, umax = 0u;
+#pragma unroll
+      for (int i = 7; i >= 0; --i) {
+        const int r = 8 * g + i;
+        const uint32_t h = (uint32_t)__double2hiint(v[Gm::pinv(r)]);
+        n[r >> 4] = __funnelshift_l(h, n[r >> 4], 1);
+        const uint32_t u = h + h;  // the high word without its sign bit, doubled
+        umin = min(umin, u);
+        umax = max(umax, u);
+      }
+      // 18.5 = 0x4032800000000000: |z| < 18.5 iff its high word is below
+      // 0x40328000 (the low word of 18.5 is zero); non-finite iff >= 0x7ff00000
+      if (umin < 2u * kSmallHi || umax >= 2u * kInfHi) gsmall |= 1u << g;
+    }
+    s0 = ~((n[1] << 16) | n[0]);
+    s1 = ~((n[3] << 16) | n[2]);
+    if (gsmall) {
+      // rare (one thread in ~60 at the BASELINE shapes): park the 64 values at
+      // their natural shared-memory positions (this thread's own block; the
+      // weights below read the small ones from there) and walk the flagged
+      // groups -- small bits, the sign of a -0.0 (z >= 0 holds for it,
+      // lookup.cpp:77), and the finiteness of the first h*tau outputs
+      double* own = sm + Gm::pos(64 * t);
+#pragma unroll
+      for (int r = 0; r < 64; r += 2)
+        *reinterpret_cast<double2*>(own + r) = make_double2(v[Gm::pinv(r)], v[Gm::pinv(r + 1)]);
+      const int lim = p.code_width - 64 * t;  // outputs r < lim are code bits
+#pragma unroll 1
+      for (int g = 0; g < 8; ++g) {
+        if (!((gsmall >> g) & 1u)) continue;
+        uint4 w4[4];  // (low, high) words of the group's eight values
+#pragma unroll
+        for (int i = 0; i < 4; ++i) w4[i] = *reinterpret_cast<const uint4*>(own + 8 * g + 2 * i);
+        uint32_t mb = 0u, zb = 0u, nb = 0u;  // small, exact zero, NaN bits of the group
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint32_t lo = (i & 1) ? w4[i >> 1].z : w4[i >> 1].x;
+          const uint32_t hi = (i & 1) ? w4[i >> 1].w : w4[i >> 1].y;
+          const uint32_t habs = hi & 0x7fffffffu;
+          if (habs < kSmallHi) mb |= 1u << i;
+          if ((habs | lo) == 0u) zb |= 1u << i;
+          if (habs >= kInfHi) {
+            if (8 * g + i < lim) bad |= 2;
+            if (habs > kInfHi || lo != 0u) nb |= 1u << i;  // NaN: z >= 0 is false whatever its sign bit
+          }
+        }
+        const int sh = (8 * g) & 31;
+        if (g < 4) { m0 |= mb << sh; s0 = (s0 | (zb << sh)) & ~(nb << sh); }
+        else { m1 |= mb << sh; s1 = (s1 | (zb << sh)) & ~(nb << sh); }
+      }
+    }
   }
-  if (!fin) bad |= 2;
   // words 2t, 2t+1 hold indices 64 t .. 64 t + 63
   reinterpret_cast<uint2*>(words)[t] = make_uint2(s0, s1);
   reinterpret_cast<uint2*>(words + Gm::WORDS)[t] = make_uint2(m0, m1);
-  // the z of every small coordinate, at its natural shared-memory position
-  if ((m0 | m1) != 0u) {
-#pragma unroll
-    for (int r = 0; r < 64; ++r)
-      if ((((r < 32 ? m0 : m1) >> (r & 31)) & 1u) != 0u) sm[Gm::pos(64 * t + r)] = v[r];
-  }
   token_sync();
   const int hl = p.ke - p.kb;
   const int tau = p.tau;
   const uint32_t cmask = tau >= 32 ? 0xffffffffu : ((1u << tau) - 1u);
+#pragma unroll 1
   for (int k = p.kb + t; k < p.ke; k += TPT) {
     const int o = k * tau;
     const int wi = o >> 5, sh = o & 31;
@@ -258,6 +372,7 @@ __global__ void __launch_bounds__(128, 3) hash_sf_kernel(HashSfParams p) {
     if (small) {
       // w /= 1 + exp(-2|z_j|) over the small j ascending (lookup.cpp:185-189;
       // the other factors are exactly 1.0)
+#pragma unroll 1
       for (int j = 0; j < tau; ++j)
         if ((small >> j) & 1u) w = __ddiv_rn(w, sf_one_plus_exp_m2(fabs(sm[Gm::pos(o + j)])));
     }

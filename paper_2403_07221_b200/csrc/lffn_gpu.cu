@@ -524,6 +524,7 @@ int launch_hash_top1(lffn_ctx* c, const float* d_x, int64_t n, uint32_t* codes, 
     q.kb = int(c->kb);
     q.ke = int(c->ke);
     q.masks = c->d_sfmask;
+    q.transforms = 3;
     q.codes = codes;
     q.coeff = coeff;
     q.flag = c->d_flag;
@@ -534,8 +535,18 @@ int launch_hash_top1(lffn_ctx* c, const float* d_x, int64_t n, uint32_t* codes, 
       set_smem(reinterpret_cast<const void*>(kernel), int(smem));
       kernel<<<unsigned((n + tpb - 1) / tpb), 128, smem, st>>>(q);
     };
-    if (c->logD == 11) gof(hash_sf_kernel<11>, 11);
-    else gof(hash_sf_kernel<12>, 12);
+    // instantiated per class of live (non-padding) registers of the start layout
+    const int live = sf_live_class(int(c->logD), q.d_in);
+    if (c->logD == 11) {
+      if (live == 16) gof(hash_sf_kernel<11, 16>, 11);
+      else if (live == 24) gof(hash_sf_kernel<11, 24>, 11);
+      else if (live == 32) gof(hash_sf_kernel<11, 32>, 11);
+      else if (live == 48) gof(hash_sf_kernel<11, 48>, 11);
+      else gof(hash_sf_kernel<11, 64>, 11);
+    } else {
+      if (live == 32) gof(hash_sf_kernel<12, 32>, 12);
+      else gof(hash_sf_kernel<12, 64>, 12);
+    }
     ++c->launches;
     LFFN_CUDA(cudaGetLastError());
     return LFFN_OK;
