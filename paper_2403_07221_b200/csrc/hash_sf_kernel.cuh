@@ -79,6 +79,13 @@ struct HashSfParams {
   int* flag;
 };
 
+// threads per CTA: 64 (six CTAs, twelve warps per SM at 168 registers).  Measured
+// c2 / c3 / c4: 128 threads 0.100 / 0.346 / 0.127 ms, 64 threads 0.098 /
+// 0.338 / 0.119 ms, one token per CTA 0.098 / 0.346 / 0.119 ms; a persistent
+// grid-stride loop over tokens (all warps in the same phase at the same
+// time) 0.125 / 0.442 / 0.148 ms.
+__host__ __device__ constexpr int sf_threads(int) { return 64; }
+
 template <int LOGD>
 struct SfGeom {
   static constexpr int D = 1 << LOGD;
@@ -216,10 +223,10 @@ __host__ __device__ constexpr int sf_live_class(int logd, int d_in) {
 }
 
 template <int LOGD, int LIVE>
-__global__ void __launch_bounds__(128, 3) hash_sf_kernel(HashSfParams p) {
+__global__ void __launch_bounds__(sf_threads(LOGD), 384 / sf_threads(LOGD)) hash_sf_kernel(HashSfParams p) {
   using Gm = SfGeom<LOGD>;
   constexpr int TPT = Gm::TPT;
-  constexpr int TPB = 128 / TPT;  // tokens per CTA
+  constexpr int TPB = sf_threads(LOGD) / TPT;  // tokens per CTA
   extern __shared__ double smem[];
   // per token: PAD doubles of transpose buffer, then 2 * WORDS sign / small words
   constexpr int SLOT = Gm::PAD + Gm::WORDS;  // doubles (the words take WORDS doubles)

@@ -529,11 +529,11 @@ int launch_hash_top1(lffn_ctx* c, const float* d_x, int64_t n, uint32_t* codes, 
     q.coeff = coeff;
     q.flag = c->d_flag;
     auto gof = [&](auto kernel, int logd) {
-      const int tpt = (1 << logd) / 64, tpb = 128 / tpt;
+      const int tpt = (1 << logd) / 64, tpb = sf_threads(logd) / tpt;
       const int slot = (1 << logd) + 2 * ((1 << logd) >> 6) + (1 << logd) / 32;
       const size_t smem = size_t(tpb) * size_t(slot) * sizeof(double);
       set_smem(reinterpret_cast<const void*>(kernel), int(smem));
-      kernel<<<unsigned((n + tpb - 1) / tpb), 128, smem, st>>>(q);
+      kernel<<<unsigned((n + tpb - 1) / tpb), sf_threads(logd), smem, st>>>(q);
     };
     // instantiated per class of live (non-padding) registers of the start layout
     const int live = sf_live_class(int(c->logD), q.d_in);

@@ -466,6 +466,9 @@ K1F_SHAPES = [
     (770, 32, 200, 7, 50),        # d_in % 4 != 0 (scalar x loads), tau 7
     (2048, 32, 91, 22, 40),       # tau 22 spanning words, h*tau = 2002
     (3000, 8, 100, 24, 33),       # D = 4096, d_in % 64 != 0
+    (1300, 16, 128, 16, 45),      # D = 2048, 41 of 64 start registers live (class 48)
+    (500, 16, 250, 8, 37),        # D = 2048, 16 live start registers, ragged tail (d_in % 32 != 0)
+    (1500, 16, 300, 8, 35),       # D = 4096 from h*tau = 2400, 24 of 64 start registers live (class 32)
 ]
 
 
@@ -484,8 +487,12 @@ def test_production_signflip_hash(oracle, shape):
     proj = Projection.init(ProjectionSpec(d_in, h * tau, ProjKind.signflip), 1)
     x = gaussian_matrix(n, d_in, 0).astype(np.float32)
     x[1] *= 1e-30  # a tiny token: many small |z| (weights below 1)
+    x[2] = 0.0     # z = +-0.0 everywhere: every code bit is set (z >= 0, lookup.cpp:77)
+    x[3] = -0.0
+    x[4, : d_in // 2] = 0.0  # partly zero: exact zeros beside ordinary values
     layer = LookupFFN(cfg, proj, None, max_tokens=n)
     codes, coeff, _ = device_hash(layer, x, want_z=False)
+    assert (codes[2] == (1 << tau) - 1).all() and (codes[3] == (1 << tau) - 1).all()
     c, s = to_oracle(cfg, proj)
     z_ref = oracle.proj_forward(s, proj.blob, x.astype(np.float64))
     codes_ref = assert_codes_match(codes, z_ref, h, tau, "K1f")
