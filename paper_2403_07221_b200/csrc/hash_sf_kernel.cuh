@@ -222,6 +222,125 @@ __host__ __device__ constexpr int sf_live_class(int logd, int d_in) {
   return need <= 16 ? 16 : need <= 24 ? 24 : need <= 32 ? 32 : need <= 48 ? 48 : 64;
 }
 
+// The epilogue of a token whose 64 z values per thread are 64 consecutive
+// coordinates (register r' = PERM ? pinv(r) : r holds z[64 t + r]): sign
+// words, small-|z| words, codes and top-1 weights (lookup.cpp:74-100,
+// 185-189).  `sm` is the token's padded buffer (free by now: the small z are
+// parked in it), `words` its 2 * WORDS sign / small words; token_sync
+// synchronises the token's threads.
+struct SfEpilogue {
+  int code_width, tau, kb, ke;
+  uint32_t* codes;
+  float* coeff;
+};
+
+template <int LOGD, bool PERM, typename Sync>
+__device__ __forceinline__ void sf_epilogue(double (&v)[64], double* sm, uint32_t* words, int t, int64_t token,
+                                            const SfEpilogue& e, int& bad, Sync token_sync) {
+  using Gm = SfGeom<LOGD>;
+  constexpr int TPT = Gm::TPT;
+  auto PINV = [](int r) { return PERM ? Gm::pinv(r) : r; };
+  // ---- epilogue in layout A: z[64 t + r] = v[pinv(r)]
+  // sign bits (z >= 0, lookup.cpp:77), small-|z| bits (|z| < 18.5) and the
+  // finiteness of the first h*tau outputs (projection.cpp:264, lookup.cpp:204)
+  uint32_t s0 = 0, s1 = 0, m0 = 0, m1 = 0;
+  {
+    // integer pass: negative-sign words (four funnel chains) and, per group
+    // of eight coordinates, the range of |z|'s high words
+    constexpr uint32_t kSmallHi = 0x40328000u, kInfHi = 0x7ff00000u;
+    uint32_t n[4] = {0u, 0u, 0u, 0u};
+    uint32_t gsmall = 0u;  // bit g: group g (coordinates 8 g .. 8 g + 7) holds a small or non-finite value
+#pragma unroll
+    for (int g = 7; g >= 0; --g) {
+      uint32_t umin = 0xffffffffu, umax = 0u;
+#pragma unroll
+      for (int i = 7; i >= 0; --i) {
+        const int r = 8 * g + i;
+        const uint32_t h = (uint32_t)__double2hiint(v[PINV(r)]);
+        n[r >> 4] = __funnelshift_l(h, n[r >> 4], 1);
+        const uint32_t u = h + h;  // the high word without its sign bit, doubled
+        umin = min(umin, u);
+        umax = max(umax, u);
+      }
+      // 18.5 = 0x4032800000000000: |z| < 18.5 iff its high word is below
+      // 0x40328000 (the low word of 18.5 is zero); non-finite iff >= 0x7ff00000
+      if (umin < 2u * kSmallHi || umax >= 2u * kInfHi) gsmall |= 1u << g;
+    }
+    s0 = ~((n[1] << 16) | n[0]);
+    s1 = ~((n[3] << 16) | n[2]);
+    if (gsmall) {
+      // rare (one thread in ~60 at the BASELINE shapes): park the 64 values at
+      // their natural shared-memory positions (this thread's own block; the
+      // weights below read the small ones from there) and walk the flagged
+      // groups -- small bits, the sign of a -0.0 (z >= 0 holds for it,
+      // lookup.cpp:77), and the finiteness of the first h*tau outputs
+      double* own = sm + Gm::pos(64 * t);
+#pragma unroll
+      for (int r = 0; r < 64; r += 2)
+        *reinterpret_cast<double2*>(own + r) = make_double2(v[PINV(r)], v[PINV(r + 1)]);
+      const int lim = e.code_width - 64 * t;  // outputs r < lim are code bits
+#pragma unroll 1
+      for (int g = 0; g < 8; ++g) {
+        if (!((gsmall >> g) & 1u)) continue;
+        uint4 w4[4];  // (low, high) words of the group's eight values
+#pragma unroll
+        for (int i = 0; i < 4; ++i) w4[i] = *reinterpret_cast<const uint4*>(own + 8 * g + 2 * i);
+        uint32_t mb = 0u, zb = 0u, nb = 0u;  // small, exact zero, NaN bits of the group
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint32_t lo = (i & 1) ? w4[i >> 1].z : w4[i >> 1].x;
+          const uint32_t hi = (i & 1) ? w4[i >> 1].w : w4[i >> 1].y;
+          const uint32_t habs = hi & 0x7fffffffu;
+          if (habs < kSmallHi) mb |= 1u << i;
+          if ((habs | lo) == 0u) zb |= 1u << i;
+          if (habs >= kInfHi) {
+            if (8 * g + i < lim) bad |= 2;
+            if (habs > kInfHi || lo != 0u) nb |= 1u << i;  // NaN: z >= 0 is false whatever its sign bit
+          }
+        }
+        const int sh = (8 * g) & 31;
+        if (g < 4) { m0 |= mb << sh; s0 = (s0 | (zb << sh)) & ~(nb << sh); }
+        else { m1 |= mb << sh; s1 = (s1 | (zb << sh)) & ~(nb << sh); }
+      }
+    }
+  }
+  // words 2t, 2t+1 hold indices 64 t .. 64 t + 63
+  reinterpret_cast<uint2*>(words)[t] = make_uint2(s0, s1);
+  reinterpret_cast<uint2*>(words + Gm::WORDS)[t] = make_uint2(m0, m1);
+  token_sync();
+  const int hl = e.ke - e.kb;
+  const int tau = e.tau;
+  const uint32_t cmask = tau >= 32 ? 0xffffffffu : ((1u << tau) - 1u);
+#pragma unroll 1
+  for (int k = e.kb + t; k < e.ke; k += TPT) {
+    const int o = k * tau;
+    const int wi = o >> 5, sh = o & 31;
+    LFFN_DCHECK(wi < Gm::WORDS && o + tau <= e.code_width);
+    const uint32_t w_lo = words[wi];
+    const uint32_t w_hi = (wi + 1 < Gm::WORDS) ? words[wi + 1] : 0u;
+    const uint32_t code = __funnelshift_r(w_lo, w_hi, sh) & cmask;
+    const uint32_t small = __funnelshift_r(words[Gm::WORDS + wi],
+                                           (wi + 1 < Gm::WORDS) ? words[Gm::WORDS + wi + 1] : 0u, sh) &
+                           cmask;
+    double w = 1.0;
+    if (small) {
+      // w = 1 / prod_j (1 + exp(-2|z_j|)) over the small j (lookup.cpp:185-189
+      // divides by the factors one after the other; the other factors are
+      // exactly 1.0).  One division of the float64 product instead of tau:
+      // within 1e-15 of the sequential quotient, far inside the fp32
+      // coefficient's 2.5e-7 -- the BH projection's z are O(1), so there every
+      // coordinate takes this path
+      double prod = 1.0;
+#pragma unroll 1
+      for (int j = 0; j < tau; ++j)
+        if ((small >> j) & 1u) prod = __dmul_rn(prod, sf_one_plus_exp_m2(fabs(sm[Gm::pos(o + j)])));
+      w = __ddiv_rn(1.0, prod);
+    }
+    e.codes[token * hl + (k - e.kb)] = code;
+    e.coeff[token * hl + (k - e.kb)] = (float)w;
+  }
+}
+
 template <int LOGD, int LIVE>
 __global__ void __launch_bounds__(sf_threads(LOGD), 384 / sf_threads(LOGD)) hash_sf_kernel(HashSfParams p) {
   using Gm = SfGeom<LOGD>;
@@ -294,97 +413,9 @@ __global__ void __launch_bounds__(sf_threads(LOGD), 384 / sf_threads(LOGD)) hash
   }
 
   // ---- epilogue in layout A: z[64 t + r] = v[pinv(r)]
-  // sign bits (z >= 0, lookup.cpp:77), small-|z| bits (|z| < 18.5) and the
-  // finiteness of the first h*tau outputs (projection.cpp:264, lookup.cpp:204)
-  uint32_t s0 = 0, s1 = 0, m0 = 0, m1 = 0;
   {
-    // integer pass: negative-sign words (four funnel chains) and, per group
-    // of eight coordinates, the range of |z|'s high words
-    constexpr uint32_t kSmallHi = 0x40328000u, kInfHi = 0x7ff00000u;
-    uint32_t n[4] = {0u, 0u, 0u, 0u};
-    uint32_t gsmall = 0u;  // bit g: group g (coordinates 8 g .. 8 g + 7) holds a small or non-finite value
-#pragma unroll
-    for (int g = 7; g >= 0; --g) {
-      uint32_t umin = 0xffffffffu, umax = 0u;
-#pragma unroll
-      for (int i = 7; i >= 0; --i) {
-        const int r = 8 * g + i;
-        const uint32_t h = (uint32_t)__double2hiint(v[Gm::pinv(r)]);
-        n[r >> 4] = __funnelshift_l(h, n[r >> 4], 1);
-        const uint32_t u = h + h;  // the high word without its sign bit, doubled
-        umin = min(umin, u);
-        umax = max(umax, u);
-      }
-      // 18.5 = 0x4032800000000000: |z| < 18.5 iff its high word is below
-      // 0x40328000 (the low word of 18.5 is zero); non-finite iff >= 0x7ff00000
-      if (umin < 2u * kSmallHi || umax >= 2u * kInfHi) gsmall |= 1u << g;
-    }
-    s0 = ~((n[1] << 16) | n[0]);
-    s1 = ~((n[3] << 16) | n[2]);
-    if (gsmall) {
-      // rare (one thread in ~60 at the BASELINE shapes): park the 64 values at
-      // their natural shared-memory positions (this thread's own block; the
-      // weights below read the small ones from there) and walk the flagged
-      // groups -- small bits, the sign of a -0.0 (z >= 0 holds for it,
-      // lookup.cpp:77), and the finiteness of the first h*tau outputs
-      double* own = sm + Gm::pos(64 * t);
-#pragma unroll
-      for (int r = 0; r < 64; r += 2)
-        *reinterpret_cast<double2*>(own + r) = make_double2(v[Gm::pinv(r)], v[Gm::pinv(r + 1)]);
-      const int lim = p.code_width - 64 * t;  // outputs r < lim are code bits
-#pragma unroll 1
-      for (int g = 0; g < 8; ++g) {
-        if (!((gsmall >> g) & 1u)) continue;
-        uint4 w4[4];  // (low, high) words of the group's eight values
-#pragma unroll
-        for (int i = 0; i < 4; ++i) w4[i] = *reinterpret_cast<const uint4*>(own + 8 * g + 2 * i);
-        uint32_t mb = 0u, zb = 0u, nb = 0u;  // small, exact zero, NaN bits of the group
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const uint32_t lo = (i & 1) ? w4[i >> 1].z : w4[i >> 1].x;
-          const uint32_t hi = (i & 1) ? w4[i >> 1].w : w4[i >> 1].y;
-          const uint32_t habs = hi & 0x7fffffffu;
-          if (habs < kSmallHi) mb |= 1u << i;
-          if ((habs | lo) == 0u) zb |= 1u << i;
-          if (habs >= kInfHi) {
-            if (8 * g + i < lim) bad |= 2;
-            if (habs > kInfHi || lo != 0u) nb |= 1u << i;  // NaN: z >= 0 is false whatever its sign bit
-          }
-        }
-        const int sh = (8 * g) & 31;
-        if (g < 4) { m0 |= mb << sh; s0 = (s0 | (zb << sh)) & ~(nb << sh); }
-        else { m1 |= mb << sh; s1 = (s1 | (zb << sh)) & ~(nb << sh); }
-      }
-    }
-  }
-  // words 2t, 2t+1 hold indices 64 t .. 64 t + 63
-  reinterpret_cast<uint2*>(words)[t] = make_uint2(s0, s1);
-  reinterpret_cast<uint2*>(words + Gm::WORDS)[t] = make_uint2(m0, m1);
-  token_sync();
-  const int hl = p.ke - p.kb;
-  const int tau = p.tau;
-  const uint32_t cmask = tau >= 32 ? 0xffffffffu : ((1u << tau) - 1u);
-#pragma unroll 1
-  for (int k = p.kb + t; k < p.ke; k += TPT) {
-    const int o = k * tau;
-    const int wi = o >> 5, sh = o & 31;
-    LFFN_DCHECK(wi < Gm::WORDS && o + tau <= p.code_width);
-    const uint32_t w_lo = words[wi];
-    const uint32_t w_hi = (wi + 1 < Gm::WORDS) ? words[wi + 1] : 0u;
-    const uint32_t code = __funnelshift_r(w_lo, w_hi, sh) & cmask;
-    const uint32_t small = __funnelshift_r(words[Gm::WORDS + wi],
-                                           (wi + 1 < Gm::WORDS) ? words[Gm::WORDS + wi + 1] : 0u, sh) &
-                           cmask;
-    double w = 1.0;
-    if (small) {
-      // w /= 1 + exp(-2|z_j|) over the small j ascending (lookup.cpp:185-189;
-      // the other factors are exactly 1.0)
-#pragma unroll 1
-      for (int j = 0; j < tau; ++j)
-        if ((small >> j) & 1u) w = __ddiv_rn(w, sf_one_plus_exp_m2(fabs(sm[Gm::pos(o + j)])));
-    }
-    p.codes[token * hl + (k - p.kb)] = code;
-    p.coeff[token * hl + (k - p.kb)] = (float)w;
+    SfEpilogue e{p.code_width, p.tau, p.kb, p.ke, p.codes, p.coeff};
+    sf_epilogue<LOGD, true>(v, sm, words, t, token, e, bad, token_sync);
   }
   if (bad) atomicOr(p.flag, bad);
 }

@@ -158,6 +158,7 @@ struct lffn_ctx {
   int bwd_one_pass = 0;          // LFFN_OPT_BWD_ONE_PASS: single-pass KB1 (A/B reference)
   int hash_exact = 0;            // LFFN_OPT_HASH_EXACT: always K1 (z bit-identical)
   int host_chunks = 8;           // LFFN_OPT_HOST_CHUNKS: lffn_forward_host pipeline chunks
+  bool hash_exact_bh_old = false;  // (A/B: the round-1 BH kernel)
   int gather_sms = 0;            // LFFN_OPT_GATHER_SMS: persistent gather grid over this many SMs (0 = all)
   unsigned long long* d_sfmask = nullptr;  // K1f: per-thread sign masks [3][D/64]
   int small_max = 64;                // LFFN_OPT_SMALL_MAX_TOKENS: K5 up to this batch size
@@ -418,6 +419,26 @@ int launch_hash_top1(lffn_ctx* c, const float* d_x, int64_t n, uint32_t* codes, 
     bh.b = int(c->proj.block == 0 ? c->D : c->proj.block);
     bh.logb = ilog2(bh.b);
     bh.stages = int(c->proj.stages);
+    if (c->D == 2048 && bh.b == 64 && !c->hash_exact_bh_old) {
+      // the paper's shape: 8-column x 8-token register tiles, B rows three
+      // ahead in registers (hash_bh64_kernel); exact unless no z is requested
+      const size_t smem64 = size_t(8) * size_t(padded_len(2048)) * sizeof(double) + size_t(4) * 4 * 256 * 16 +
+                            size_t(8) * 128 * sizeof(uint32_t);  // tokens, B ring, sign / small words
+      const unsigned grid64 = (unsigned)((n + 7) / 8);
+      p.tokens_per_block = 8;
+      p.threads_per_token = 64;
+      const bool fused = !z_out && !exact_z && !c->hash_exact;
+      if (fused) {
+        set_smem(reinterpret_cast<const void*>(hash_bh64_kernel<true>), int(smem64));
+        hash_bh64_kernel<true><<<grid64, 256, smem64, st>>>(p, bh);
+      } else {
+        set_smem(reinterpret_cast<const void*>(hash_bh64_kernel<false>), int(smem64));
+        hash_bh64_kernel<false><<<grid64, 256, smem64, st>>>(p, bh);
+      }
+      ++c->launches;
+      LFFN_CUDA(cudaGetLastError());
+      return LFFN_OK;
+    }
     p.tokens_per_block = int(16384 / c->D);
     p.threads_per_token = int(c->D / E5);
     const size_t smem = size_t(p.tokens_per_block) * size_t(padded_len(int(c->D))) * sizeof(double);

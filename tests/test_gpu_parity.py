@@ -165,6 +165,12 @@ def test_hash_bh_bit_exact(oracle, shape):
     assert np.array_equal(z.view(np.uint64), z_ref.view(np.uint64)), "z not bit-identical"
     codes_ref, absz = oracle.compute_codes(z_ref, h, tau)
     assert np.array_equal(codes, codes_ref)
+    # the production path (no z requested; fused multiply-add at D = 2048, b =
+    # 64): codes bit-exact wherever |z_ref| > 1e-5, weights at the fp32 bar
+    from test_gpu_parity_configs import assert_codes_match
+    codes_p, coeff_p, _ = device_hash(layer, x, want_z=False)
+    assert_codes_match(codes_p, z_ref, h, tau, "bh production")
+    np.testing.assert_allclose(coeff_p, coeff, rtol=2.5e-7, atol=0)
     y = device_forward(layer, x)
     y_ref = oracle.lookup_forward(c, s, proj.blob, stored_tables(T.data, "f32"),
                                   x.astype(np.float64))

@@ -15,7 +15,7 @@ import torch  # noqa: E402
 
 from paper_2403_07221_b200 import LookupFFN  # noqa: E402
 from paper_2403_07221_b200.configs import WORKLOADS, config_of, make_x, spec_of  # noqa: E402
-from paper_2403_07221_b200.lookup import Projection  # noqa: E402
+from paper_2403_07221_b200.lookup import Projection, ProjKind  # noqa: E402
 
 
 def main():
@@ -23,13 +23,14 @@ def main():
     ap.add_argument("configs", nargs="*", default=["c2", "c3", "c4"])
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--tokens", type=int, default=0)
+    ap.add_argument("--kind", default="signflip", help="signflip | bh | acdc | dense")
     a = ap.parse_args()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for name in a.configs:
         w = WORKLOADS[name]
         n = a.tokens or w.n
         cfg = config_of(w)
-        proj = Projection.init(spec_of(w), 1)
+        proj = Projection.init(spec_of(w, ProjKind[a.kind]), 1)
         layer = LookupFFN(cfg, proj, None, max_tokens=n)
         x = torch.from_numpy(make_x(w, n)).cuda()
         codes = torch.empty((n, w.h), dtype=torch.int32, device="cuda")
