@@ -38,9 +38,13 @@ python tools/small_once.py 1 64 > $out/${tag}_plain_small.log 2>&1 && \
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:forward_small -s 2 -c 2 \
   -o $out/${tag}_prof_small -f python tools/small_once.py 1 64 > $out/${tag}_ncu_small.log 2>&1
 echo "prof small rc=$?"
+python bench.py --kind bh --steps 1 --warmup 3 --no-cpu-baseline > $out/${tag}_plain_bh.log 2>&1 && \
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:hash_bh64 -s 2 -c 1 \
+  -o $out/${tag}_prof_bh -f python bench.py --kind bh --steps 1 --warmup 3 --no-cpu-baseline > $out/${tag}_ncu_bh.log 2>&1
+echo "prof bh rc=$?"
 # summaries on the box (the .ncu-rep files exceed gpurun's copy-back limit)
 python tools/ncu_summary.py launches $out/${tag}_launches.csv > $out/${tag}_launches.md 2>&1
-for r in prof prof_c3 prof_small; do
+for r in prof prof_c3 prof_small prof_bh; do
   python tools/ncu_summary.py full $out/${tag}_$r.ncu-rep > $out/${tag}_$r.md 2>&1
   ncu -i $out/${tag}_$r.ncu-rep --page raw --csv > $out/${tag}_$r.raw.csv 2>/dev/null
 done
