@@ -149,6 +149,7 @@ BH_SHAPES = [
     (50, 30, 12, 10, 33, 4, 16),       # non-pow2 pad + truncate (D = 128)
     (3, 5, 1, 2, 7, 1, 0),             # D = 4, one full-width block
     (1024, 1024, 128, 10, 16, 4, 64),  # c3 width (truncating h*tau = 1280 of D = 2048)
+    (700, 16, 250, 8, 13, 3, 64),      # D = 2048, b = 64: ragged last CTA (13 of 16 token slots), d_in % 32 != 0
     (4096, 64, 512, 8, 6, 2, 32),      # D = 4096
 ]
 
