@@ -33,7 +33,7 @@ def digest(a: np.ndarray) -> str:
 
 
 def case(ref, name, cfg, spec, n, *, x_seed, proj_seed, t_seed, t_std, x32=True, blob=None,
-         tables=None, x=None, store_tables=True):
+         tables=None, x=None, store_tables=True, compact=False):
     if blob is None:
         blob = ref.proj_init(spec, proj_seed)
     if tables is None:
@@ -53,6 +53,17 @@ def case(ref, name, cfg, spec, n, *, x_seed, proj_seed, t_seed, t_std, x32=True,
     )
     if store_tables:
         rec["T"] = tables
+    if compact:
+        # BASELINE-width cases: z (n x D float64) is pinned by its sha256, the
+        # all-ones dots are dropped, x is stored as the fp32 values it holds
+        rec["z_sha256"] = digest(rec.pop("z"))
+        rec["z_shape"] = np.array(cache["z"].shape)
+        rec["x"] = x.astype(np.float32)
+        if blob.nbytes > (1 << 18):
+            # large parameter blobs (BH blocks) regenerate from proj_seed
+            rec["blob_sha256"] = digest(rec.pop("blob"))
+        if cfg.variant not in (SCALED,):
+            rec.pop("dots")
     np.savez_compressed(os.path.join(OUT, name + ".npz"), **rec)
     print(f"{name}: n={n} y[0,:3]={y[0, :3]}")
 
@@ -85,6 +96,34 @@ def main():
     x = (x - x.mean(axis=1, keepdims=True)) / x.std(axis=1, keepdims=True)
     case(ref, "c2_signflip_4tok", c2, c2.spec(SIGNFLIP), 4, x_seed=0, proj_seed=1, t_seed=2,
          t_std=0.02, x=x, store_tables=False)
+    # Round 2: the other BASELINE widths with enough tokens (> 64) to take the
+    # production kernels (K1f + the persistent / split gathers) instead of the
+    # one-launch small-batch path.  Compact records (z by checksum).
+    n2 = 72
+    x = ref.gaussian(0, n2 * 768).reshape(n2, 768)
+    x = (x - x.mean(axis=1, keepdims=True)) / x.std(axis=1, keepdims=True)
+    t2 = ref.gaussian(2, 256 * 256 * 768, 0.02)
+    case(ref, "c2_signflip_72tok", c2, c2.spec(SIGNFLIP), n2, x_seed=0, proj_seed=1, t_seed=2,
+         t_std=0.02, x=x, tables=t2, store_tables=False, compact=True)
+    # c5: skewed tokens x = U z + 0.01 eps (U <- make_rng(0), draws <- make_rng(100))
+    U = ref.gaussian(0, 768 * 4).reshape(768, 4)
+    draws = ref.gaussian(100, n2 * (4 + 768)).reshape(n2, 4 + 768)
+    xs = draws[:, :4] @ U.T + 0.01 * draws[:, 4:]
+    case(ref, "c5_skew_72tok", c2, c2.spec(SIGNFLIP), n2, x_seed=100, proj_seed=1, t_seed=2,
+         t_std=0.02, x=xs, tables=t2, store_tables=False, compact=True)
+    # c2 with the paper's BH4 (b = 64)
+    case(ref, "c2_bh4_40tok", c2, c2.spec(BH, stages=4, block=64), 40, x_seed=0, proj_seed=1,
+         t_seed=2, t_std=0.02, x=x[:40], tables=t2, store_tables=False, compact=True)
+    del t2
+    # c3 width (tau = 10, h * tau = 1280 of D = 2048) with a narrow output
+    # (d_out = 64: the 1024-wide stack would be 1 GB of float64)
+    c3w = Cfg(1024, 64, 128, 10)
+    case(ref, "c3w_signflip_72tok", c3w, c3w.spec(SIGNFLIP), n2, x_seed=0, proj_seed=1, t_seed=2,
+         t_std=0.02, store_tables=False, compact=True)
+    # c4 width (D = 4096, two warps per token in the hash), narrow output
+    c4w = Cfg(4096, 64, 512, 8)
+    case(ref, "c4w_signflip_40tok", c4w, c4w.spec(SIGNFLIP), 40, x_seed=0, proj_seed=1, t_seed=2,
+         t_std=0.02, store_tables=False, compact=True)
 
 
 if __name__ == "__main__":
