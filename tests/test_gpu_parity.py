@@ -517,6 +517,62 @@ def test_production_signflip_hash(oracle, shape):
     assert np.array_equal(coeff_s, coeff[:, kb:ke])
 
 
+def _random_k1f_shapes(count, seed):
+    """Seeded random (d_in, h, tau, n) whose transform width is 2048 or 4096."""
+    rng = np.random.default_rng(seed)
+    shapes = []
+    while len(shapes) < count:
+        tau = int(rng.integers(1, 25))
+        logd = int(rng.choice([11, 12]))
+        D = 1 << logd
+        lo = D // 2 + 1
+        width = int(rng.integers(lo, D + 1))          # max(d_in, h * tau) in (D/2, D]
+        if rng.random() < 0.5:                         # the width comes from h * tau
+            h = max(1, width // tau)
+            if h * tau <= D // 2:
+                continue
+            d_in = int(rng.integers(1, D + 1))
+            if max(d_in, h * tau) > D:
+                continue
+        else:                                          # the width comes from d_in
+            d_in = width
+            h = int(rng.integers(1, max(2, D // tau)))
+            if h * tau > D:
+                continue
+        shapes.append((d_in, 8, h, tau, int(rng.integers(17, 90))))
+    return shapes
+
+
+@pytest.mark.parametrize("shape", _random_k1f_shapes(14, 20240307), ids=lambda s: "x".join(map(str, s)))
+def test_production_signflip_hash_random_shapes(oracle, shape):
+    """Seeded random widths, table counts, code sizes and batch sizes through
+    K1f: every live-register class, code words straddling sign words, ragged
+    last CTAs.  Codes at the north-star bar, weights at the fp32 bar, and an
+    odd table shard equal to the full range's columns."""
+    from test_gpu_parity_configs import assert_codes_match
+
+    d_in, d_out, h, tau, n = shape
+    cfg = LookupConfig(d_in=d_in, d_out=d_out, tables=h, code_bits=tau)
+    proj = Projection.init(ProjectionSpec(d_in, h * tau, ProjKind.signflip), 3)
+    x = gaussian_matrix(n, d_in, 11).astype(np.float32)
+    x[0] *= 1e-4   # small |z|: weights below 1
+    x[n - 1] = 0.0
+    layer = LookupFFN(cfg, proj, None, max_tokens=n)
+    codes, coeff, _ = device_hash(layer, x, want_z=False)
+    c, s = to_oracle(cfg, proj)
+    z_ref = oracle.proj_forward(s, proj.blob, x.astype(np.float64))
+    assert_codes_match(codes, z_ref, h, tau, "K1f random")
+    _, absz = oracle.compute_codes(z_ref, h, tau)
+    w_ref = np.array([oracle.top1_weight(a) for a in absz.reshape(-1, tau)]).reshape(n, h)
+    np.testing.assert_allclose(coeff, w_ref.astype(np.float32), rtol=2.5e-7, atol=0)
+    if h >= 3:
+        kb, ke = h // 3, h - 1
+        sh = LookupFFN(cfg, proj, None, max_tokens=n, table_range=(kb, ke))
+        codes_s, coeff_s, _ = device_hash(sh, x, want_z=False)
+        assert np.array_equal(codes_s, codes[:, kb:ke])
+        assert np.array_equal(coeff_s, coeff[:, kb:ke])
+
+
 def test_production_signflip_hash_non_finite_input():
     cfg = LookupConfig(d_in=768, d_out=8, tables=256, code_bits=8)
     proj = Projection.init(ProjectionSpec(768, 2048, ProjKind.signflip), 1)
