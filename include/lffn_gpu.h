@@ -248,7 +248,12 @@ int lffn_sync(lffn_ctx* ctx, void* stream);
  *                              in one launch spread over (token, table
  *                              group) CTAs (signflip, D = 2048, top-1)
  *   LFFN_OPT_GATHER_SMS        persistent gather grid over this many SMs
- *                              (0 = all, the default) */
+ *                              (0 = all, the default)
+ *   LFFN_OPT_HOST_DIRECT       1 (default) = lffn_forward_host on a small
+ *                              batch with pinned buffers writes y and the
+ *                              non-finite flag straight into host memory and
+ *                              polls the flag; 0 = the CUDA-graph path with
+ *                              copy nodes */
 #define LFFN_OPT_DENSE_EXACT 1
 #define LFFN_OPT_TABLE_GROUP_BYTES 2
 #define LFFN_OPT_GATHER_VARIANT 3
@@ -258,6 +263,7 @@ int lffn_sync(lffn_ctx* ctx, void* stream);
 #define LFFN_OPT_HOST_CHUNKS 8
 #define LFFN_OPT_SMALL_MAX_TOKENS 10
 #define LFFN_OPT_GATHER_SMS 11
+#define LFFN_OPT_HOST_DIRECT 12
 int lffn_ctx_set_option(lffn_ctx* ctx, int option, int64_t value);
 
 /* ---- multi-GPU table sharding (north star: tables split

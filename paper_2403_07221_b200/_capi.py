@@ -20,7 +20,7 @@ LFFN_F32, LFFN_BF16, LFFN_F64 = 0, 1, 2
 LFFN_OPT_DENSE_EXACT, LFFN_OPT_TABLE_GROUP_BYTES, LFFN_OPT_GATHER_VARIANT = 1, 2, 3
 LFFN_OPT_BF16_COEFF_FMA, LFFN_OPT_BWD_ONE_PASS, LFFN_OPT_HASH_EXACT, LFFN_OPT_HOST_CHUNKS = 5, 6, 7, 8
 LFFN_COMBINE_REDUCE_SCATTER, LFFN_COMBINE_ALL_REDUCE, LFFN_COMBINE_NONE = 0, 1, 2
-LFFN_OPT_SMALL_MAX_TOKENS, LFFN_OPT_GATHER_SMS = 10, 11
+LFFN_OPT_SMALL_MAX_TOKENS, LFFN_OPT_GATHER_SMS, LFFN_OPT_HOST_DIRECT = 10, 11, 12
 
 
 class lffn_cfg(C.Structure):

@@ -158,6 +158,8 @@ struct lffn_ctx {
   int bwd_one_pass = 0;          // LFFN_OPT_BWD_ONE_PASS: single-pass KB1 (A/B reference)
   int hash_exact = 0;            // LFFN_OPT_HASH_EXACT: always K1 (z bit-identical)
   int host_chunks = 8;           // LFFN_OPT_HOST_CHUNKS: lffn_forward_host pipeline chunks
+  bool host_direct = true;       // LFFN_OPT_HOST_DIRECT: small batches write y / the flag straight to pinned memory
+  int* h_flag_dev = nullptr;     // device address of h_flag
   bool hash_exact_bh_old = false;  // (A/B: the round-1 BH kernel)
   int gather_sms = 0;            // LFFN_OPT_GATHER_SMS: persistent gather grid over this many SMs (0 = all)
   unsigned long long* d_sfmask = nullptr;  // K1f: per-thread sign masks [3][D/64]
@@ -1186,6 +1188,11 @@ int lffn_ctx_create_shard(lffn_ctx** out, int device, int64_t max_tokens, const 
   CK(cudaMalloc(&c->d_xbuf, mt * size_t(cfg->d_in) * sizeof(float)));
   CK(cudaMalloc(&c->d_ybuf, mt * size_t(cfg->d_out) * sizeof(float)));
   CK(cudaMallocHost(&c->h_flag, sizeof(int)));
+  {
+    void* hfd = nullptr;
+    if (cudaHostGetDevicePointer(&hfd, c->h_flag, 0) == cudaSuccess) c->h_flag_dev = static_cast<int*>(hfd);
+    else cudaGetLastError();
+  }
   CK(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&c->s_comp2, cudaStreamNonBlocking));
@@ -1313,13 +1320,44 @@ int lffn_forward(lffn_ctx* c, const float* d_x, int64_t n, float* d_y, void* str
 
 namespace {
 
-bool is_pinned(const void* p) {
+// pinned (page-locked) host memory; *dev = the address the device uses for it
+bool is_pinned(const void* p, void** dev = nullptr) {
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
+  if (dev) *dev = a.devicePointer;
   return a.type == cudaMemoryTypeHost;
+}
+
+// Small batches through the host path without copy-engine transfers of y or
+// the flag: K5 writes y straight into the caller's pinned buffer (each
+// element once), a one-thread kernel publishes the flag, and the host polls
+// it -- no copy nodes, no driver-side synchronisation latency.  x is read in
+// place for n <= 4 (every CTA of a token's cluster re-reads its row: 16 x 3 KB
+// over PCIe per token is cheap for a few tokens only) and copied otherwise.
+int forward_host_direct(lffn_ctx* c, const float* h_x, const float* dx, int64_t n, float* dy) {
+  cudaStream_t st = c->s_comp;
+  const float* xs = dx;
+  if (n > 4) {
+    LFFN_CUDA(cudaMemcpyAsync(c->d_xbuf, h_x, size_t(n) * size_t(c->cfg.d_in) * sizeof(float),
+                              cudaMemcpyHostToDevice, st));
+    xs = c->d_xbuf;
+  }
+  volatile int* hf = c->h_flag;
+  *hf = -1;
+  if (int rc = launch_small(c, xs, n, dy, 0, st)) return rc;
+  flag_to_host_kernel<<<1, 1, 0, st>>>(c->d_flag, c->h_flag_dev);
+  LFFN_CUDA(cudaGetLastError());
+  // poll; a stuck or failed launch falls back to the driver's synchronise
+  for (int64_t spin = 0; *hf == -1; ++spin) {
+    if (spin > (int64_t(1) << 22)) {
+      LFFN_CUDA(cudaStreamSynchronize(st));
+      if (*hf == -1) return fail(LFFN_ERR_RUNTIME, "host path: flag not published");
+    }
+  }
+  return flag_message(*hf);
 }
 
 // Small batches through the host path: the whole call (x in, K5, y out, the
@@ -1391,8 +1429,13 @@ int lffn_forward_host(lffn_ctx* c, const float* h_x, int64_t n, float* h_y) {
   if (!c->d_T) return fail(LFFN_ERR_USAGE, "lookup forward: tables not uploaded");
   DeviceGuard g(c->device);
   if (n == 0) return LFFN_OK;
-  const bool pinned = is_pinned(h_x) && is_pinned(h_y);
-  if (small_eligible(c, n) && pinned) return forward_host_graph(c, h_x, n, h_y);
+  void *dx = nullptr, *dy = nullptr;
+  const bool pinned = is_pinned(h_x, &dx) && is_pinned(h_y, &dy);
+  if (small_eligible(c, n) && pinned) {
+    if (c->host_direct && dx && dy && c->h_flag_dev)
+      return forward_host_direct(c, h_x, static_cast<const float*>(dx), n, static_cast<float*>(dy));
+    return forward_host_graph(c, h_x, n, h_y);
+  }
   const int64_t d_in = c->cfg.d_in, d_out = c->cfg.d_out;
   // Chunked pipeline: H2D(chunk i+1) || compute(chunk i) || D2H(chunk i-1).
   // Structured projections use no context scratch, so consecutive chunks
@@ -1843,6 +1886,9 @@ int lffn_ctx_set_option(lffn_ctx* c, int option, int64_t value) {
       if (value < 1 || value > lffn_ctx::kChunks)
         return fail(LFFN_ERR_USAGE, "option: host chunks must be 1 .. 16");
       c->host_chunks = int(value);
+      return LFFN_OK;
+    case LFFN_OPT_HOST_DIRECT:
+      c->host_direct = value != 0;
       return LFFN_OK;
     case LFFN_OPT_BF16_COEFF_FMA:
       c->bf16w = value != 0;

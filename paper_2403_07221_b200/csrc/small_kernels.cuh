@@ -307,4 +307,13 @@ __global__ void __launch_bounds__(kSmallThreads) forward_small_kernel(SmallParam
   if (bad) atomicOr(p.flag, bad);
 }
 
+// The non-finite flag to mapped host memory, and its reset, in stream order
+// (the host path of small batches polls it: lffn_gpu.cu forward_host_direct).
+__global__ void flag_to_host_kernel(int* d_flag, volatile int* h_flag) {
+  const int f = *d_flag;
+  *d_flag = 0;
+  *h_flag = f;
+  __threadfence_system();
+}
+
 }  // namespace lffn_gpu

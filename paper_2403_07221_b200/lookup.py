@@ -489,7 +489,8 @@ class LookupFFN:
         never take the exact mixed-precision FMA path for bf16 tables),
         'bwd_one_pass' (single-pass backward table-row dot), 'hash_exact' (1 =
         the signflip hash always in the reference's stage order, z
-        bit-identical), 'host_chunks' (forward_host pipeline chunks) or
+        bit-identical), 'host_chunks' (forward_host pipeline chunks), 'host_direct'
+        (0 = small batches through the CUDA-graph copy path) or
         'small_max_tokens' (one-launch forward for batches up to this size)."""
         opt = {"dense_exact": _capi.LFFN_OPT_DENSE_EXACT,
                "table_group_bytes": _capi.LFFN_OPT_TABLE_GROUP_BYTES,
@@ -499,7 +500,8 @@ class LookupFFN:
                "hash_exact": _capi.LFFN_OPT_HASH_EXACT,
                "host_chunks": _capi.LFFN_OPT_HOST_CHUNKS,
                "small_max_tokens": _capi.LFFN_OPT_SMALL_MAX_TOKENS,
-               "gather_sms": _capi.LFFN_OPT_GATHER_SMS}[name]
+               "gather_sms": _capi.LFFN_OPT_GATHER_SMS,
+               "host_direct": _capi.LFFN_OPT_HOST_DIRECT}[name]
         check(_capi.lib().lffn_ctx_set_option(self._ctx, opt, int(value)))
 
     def launch_count(self) -> int:

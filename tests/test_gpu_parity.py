@@ -625,28 +625,35 @@ def test_small_batch_one_launch(oracle, name, n):
         assert np.array_equal(device_forward(sh, x), ys)
 
 
-def test_small_batch_host_graph_pinned():
-    """lffn_forward_host with pinned buffers and a small batch runs one CUDA
-    graph per batch size with its host pointers patched per call: equal to
-    the device entry point for new buffers, other sizes, repeated calls, and
-    still raising the stage-named NumericError."""
+@pytest.mark.parametrize("direct", [1, 0], ids=["direct", "graph"])
+def test_small_batch_host_graph_pinned(direct):
+    """lffn_forward_host with pinned buffers and a small batch: the direct
+    path (K5 writes y into the pinned buffer, a one-thread kernel publishes
+    the non-finite flag, the host polls it; x read in place up to 4 tokens)
+    and the CUDA-graph copy path (option host_direct = 0: one graph per batch
+    size with its host pointers patched per call) both equal the device
+    entry point for new buffers, other sizes, repeated calls, and still raise
+    the stage-named NumericError."""
     import torch
 
     w = WORKLOADS["c5"]
     cfg, proj, T = make_params(w)
     layer = LookupFFN(cfg, proj, T, max_tokens=64)
-    for n in (1, 8, 1, 64, 8):
+    layer.set_option("host_direct", direct)
+    for n in (1, 8, 1, 64, 8, 3, 5):
         x = make_x(w, n, seed=n)
         hx = torch.from_numpy(x).pin_memory()
         hy = torch.full((n, cfg.d_out), 7.0).pin_memory()
         layer.forward_host_ptr(hx.data_ptr(), n, hy.data_ptr())
         y_dev = device_forward(layer, x)
         assert np.array_equal(hy.numpy(), y_dev)
-    hx[0, 3] = float("nan")
-    with pytest.raises(NumericError, match="projection forward input"):
-        layer.forward_host_ptr(hx.data_ptr(), 8, hy.data_ptr())
-    hx[0, 3] = 0.0
-    layer.forward_host_ptr(hx.data_ptr(), 8, hy.data_ptr())
+    for m in (5, 2):  # copied x and x read in place
+        hx[0, 3] = float("nan")
+        with pytest.raises(NumericError, match="projection forward input"):
+            layer.forward_host_ptr(hx.data_ptr(), m, hy.data_ptr())
+        hx[0, 3] = 0.0
+        layer.forward_host_ptr(hx.data_ptr(), m, hy.data_ptr())  # the flag was reset
+        assert np.array_equal(hy.numpy()[:m], device_forward(layer, hx.numpy()[:m]))
 
 
 def test_checked_build_is_the_one_loaded():

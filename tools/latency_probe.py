@@ -56,12 +56,20 @@ for m in (1, 2, 4, 8, 12, 16, 24, 32, 48, 64, 128):
     hx = torch.from_numpy(make_x(w, m)).pin_memory()
     hy = torch.empty((m, w.d)).pin_memory()
     layer.set_option("small_max_tokens", 64)
-    ts = []
-    for r in range(60):
-        t0 = time.perf_counter()
-        layer.forward_host_ptr(hx.data_ptr(), m, hy.data_ptr())
-        if r >= 10:
-            ts.append((time.perf_counter() - t0) * 1e6)
+    host = {}
+    y_direct = None
+    for direct in (1, 0):  # y / flag written straight to pinned memory vs the CUDA-graph copy path
+        layer.set_option("host_direct", direct)
+        ts = []
+        for r in range(200):
+            t0 = time.perf_counter()
+            layer.forward_host_ptr(hx.data_ptr(), m, hy.data_ptr())
+            if r >= 20:
+                ts.append((time.perf_counter() - t0) * 1e6)
+        host[direct] = statistics.median(ts)
+        if direct:
+            y_direct = hy.clone()
+    same = bool(torch.equal(y_direct, hy))
     print(f"{name} n={m:3d}: one-launch {out[0][0]:6.1f} us warm {out[0][1]:6.1f} cold | "
-          f"two kernels {out[1][0]:6.1f} warm {out[1][1]:6.1f} cold | host path {statistics.median(ts):6.1f} us",
-          flush=True)
+          f"two kernels {out[1][0]:6.1f} warm {out[1][1]:6.1f} cold | host path direct {host[1]:6.1f} us, "
+          f"graph {host[0]:6.1f} us (same y: {same})", flush=True)
