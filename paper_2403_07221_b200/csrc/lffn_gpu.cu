@@ -159,6 +159,7 @@ struct lffn_ctx {
   int hash_exact = 0;            // LFFN_OPT_HASH_EXACT: always K1 (z bit-identical)
   int host_chunks = 8;           // LFFN_OPT_HOST_CHUNKS: lffn_forward_host pipeline chunks
   bool host_direct = true;       // LFFN_OPT_HOST_DIRECT: small batches write y / the flag straight to pinned memory
+  int64_t host_direct_max = 128; // ... and two-kernel batches up to this size (y written in place)
   int* h_flag_dev = nullptr;     // device address of h_flag
   bool hash_exact_bh_old = false;  // (A/B: the round-1 BH kernel)
   int gather_sms = 0;            // LFFN_OPT_GATHER_SMS: persistent gather grid over this many SMs (0 = all)
@@ -901,7 +902,30 @@ int forward_impl(lffn_ctx* c, const float* d_x, int64_t n, float* d_y, cudaStrea
   return LFFN_OK;
 }
 
+// Wait for everything queued on `st` and report the non-finite flag.  With
+// the flag word mapped into the device's address space a one-thread kernel
+// publishes (and resets) it in stream order and the host polls the word --
+// no copy, no driver-side synchronisation latency (~10 us per call); a queue
+// that does not drain within a few milliseconds falls back to the driver's
+// synchronise.
+int poll_flag(lffn_ctx* c, cudaStream_t st) {
+  volatile int* hf = c->h_flag;
+  for (int64_t spin = 0; *hf == -1; ++spin) {
+    if (spin > (int64_t(1) << 22)) {
+      LFFN_CUDA(cudaStreamSynchronize(st));
+      if (*hf == -1) return fail(LFFN_ERR_RUNTIME, "flag not published");
+    }
+  }
+  return flag_message(*hf);
+}
+
 int read_flag(lffn_ctx* c, cudaStream_t st) {
+  if (c->host_direct && c->h_flag_dev) {
+    *static_cast<volatile int*>(c->h_flag) = -1;
+    flag_to_host_kernel<<<1, 1, 0, st>>>(c->d_flag, c->h_flag_dev);
+    LFFN_CUDA(cudaGetLastError());
+    return poll_flag(c, st);
+  }
   LFFN_CUDA(cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
   LFFN_CUDA(cudaMemsetAsync(c->d_flag, 0, sizeof(int), st));
   LFFN_CUDA(cudaStreamSynchronize(st));
@@ -1347,17 +1371,16 @@ int forward_host_direct(lffn_ctx* c, const float* h_x, const float* dx, int64_t 
   }
   volatile int* hf = c->h_flag;
   *hf = -1;
-  if (int rc = launch_small(c, xs, n, dy, 0, st)) return rc;
+  if (small_eligible(c, n)) {
+    if (int rc = launch_small(c, xs, n, dy, 0, st)) return rc;
+  } else {
+    // medium batches: the two-kernel forward, the gather writing y in place
+    if (int rc = launch_hash(c, xs, n, c->d_codes, c->d_coeff, nullptr, st)) return rc;
+    if (int rc = launch_gather(c, c->d_codes, c->d_coeff, n, dy, 0, st)) return rc;
+  }
   flag_to_host_kernel<<<1, 1, 0, st>>>(c->d_flag, c->h_flag_dev);
   LFFN_CUDA(cudaGetLastError());
-  // poll; a stuck or failed launch falls back to the driver's synchronise
-  for (int64_t spin = 0; *hf == -1; ++spin) {
-    if (spin > (int64_t(1) << 22)) {
-      LFFN_CUDA(cudaStreamSynchronize(st));
-      if (*hf == -1) return fail(LFFN_ERR_RUNTIME, "host path: flag not published");
-    }
-  }
-  return flag_message(*hf);
+  return poll_flag(c, st);
 }
 
 // Small batches through the host path: the whole call (x in, K5, y out, the
@@ -1436,6 +1459,9 @@ int lffn_forward_host(lffn_ctx* c, const float* h_x, int64_t n, float* h_y) {
       return forward_host_direct(c, h_x, static_cast<const float*>(dx), n, static_cast<float*>(dy));
     return forward_host_graph(c, h_x, n, h_y);
   }
+  if (pinned && c->host_direct && n <= c->host_direct_max && dx && dy && c->h_flag_dev && c->nc == 1 &&
+      c->proj.kind != LFFN_PROJ_DENSE)
+    return forward_host_direct(c, h_x, static_cast<const float*>(dx), n, static_cast<float*>(dy));
   const int64_t d_in = c->cfg.d_in, d_out = c->cfg.d_out;
   // Chunked pipeline: H2D(chunk i+1) || compute(chunk i) || D2H(chunk i-1).
   // Structured projections use no context scratch, so consecutive chunks
@@ -1889,6 +1915,7 @@ int lffn_ctx_set_option(lffn_ctx* c, int option, int64_t value) {
       return LFFN_OK;
     case LFFN_OPT_HOST_DIRECT:
       c->host_direct = value != 0;
+      c->host_direct_max = value > 1 ? value : 128;
       return LFFN_OK;
     case LFFN_OPT_BF16_COEFF_FMA:
       c->bf16w = value != 0;
