@@ -391,6 +391,13 @@ __global__ void __launch_bounds__(sf_threads(LOGD), 384 / sf_threads(LOGD)) hash
   if (!active) return;  // whole tokens only: a token's threads exit together
   int bad = 0;
   double v[64];
+  // the second and third sign masks are loaded under the butterflies that
+  // precede their use (~450 cycles of L2 latency each on a token's critical
+  // path otherwise: c3 0.336 -> 0.334 ms, c4 0.117 -> 0.113) -- except in the
+  // LIVE = 24 instance (c2, c5), where the two extra live registers spill
+  // (0.096 -> 0.100 ms)
+  constexpr bool kMaskAhead = !(LOGD == 11 && LIVE == 24);
+  unsigned long long mask;
 
   // ---- x (padded to D) into layout B: register q of thread t holds
   // x[t + TPT q]; registers q >= LIVE are padding (launcher: d_in <= TPT *
@@ -433,9 +440,11 @@ __global__ void __launch_bounds__(sf_threads(LOGD), 384 / sf_threads(LOGD)) hash
     token_sync();
     sf_load_A<LOGD>(sm, v, t);
     token_sync();
+    if (kMaskAhead && tr < p.transforms) mask = __ldg(p.masks + tr * TPT + t);
     sf_stages<Gm::B2, 6>(v);
     if (tr < p.transforms) {
-      sf_flip<64>(v, __ldg(p.masks + tr * TPT + t));
+      if (!kMaskAhead) mask = __ldg(p.masks + tr * TPT + t);
+      sf_flip<64>(v, mask);
       sf_stages<0, 6>(v);
       sf_store_B<LOGD>(sm, v, t);
     }
