@@ -333,6 +333,49 @@ __device__ __forceinline__ void sf_epilogue(double (&v)[64], double* sm, uint32_
       }
     }
   }
+  if (e.tau == 8) {
+    // tau = 8 (c2, c4, c5): the thread's 64 coordinates are exactly its own
+    // eight tables 8 t .. 8 t + 7, so the codes are the bytes of its two sign
+    // words -- no exchange through shared memory, no per-table loop: two
+    // 128-bit stores of codes and two of unit weights per thread, then the
+    // rare tables with small coordinates one by one.
+    const int hl = e.ke - e.kb;
+    const int k0 = 8 * t;
+    uint32_t* crow = e.codes + token * hl - e.kb;
+    float* wrow = e.coeff + token * hl - e.kb;
+    if (k0 >= e.kb && k0 + 8 <= e.ke && (((token * hl - e.kb) & 3) == 0)) {
+      uint4* cq = reinterpret_cast<uint4*>(crow + k0);
+      cq[0] = make_uint4(s0 & 0xffu, (s0 >> 8) & 0xffu, (s0 >> 16) & 0xffu, s0 >> 24);
+      cq[1] = make_uint4(s1 & 0xffu, (s1 >> 8) & 0xffu, (s1 >> 16) & 0xffu, s1 >> 24);
+      float4* wq = reinterpret_cast<float4*>(wrow + k0);
+      wq[0] = make_float4(1.f, 1.f, 1.f, 1.f);
+      wq[1] = make_float4(1.f, 1.f, 1.f, 1.f);
+    } else {
+#pragma unroll 1
+      for (int j = 0; j < 8; ++j) {
+        const int k = k0 + j;
+        if (k < e.kb || k >= e.ke) continue;
+        crow[k] = ((j < 4 ? s0 : s1) >> (8 * (j & 3))) & 0xffu;
+        wrow[k] = 1.f;
+      }
+    }
+    if ((m0 | m1) != 0u) {
+#pragma unroll 1
+      for (int j = 0; j < 8; ++j) {
+        const int k = k0 + j;
+        const uint32_t small = ((j < 4 ? m0 : m1) >> (8 * (j & 3))) & 0xffu;
+        if (!small || k < e.kb || k >= e.ke) continue;
+        // w = 1 / prod (1 + exp(-2|z_j|)) over the small j (lookup.cpp:185-189);
+        // the values were parked in this thread's block above
+        double prod = 1.0;
+#pragma unroll 1
+        for (int b = 0; b < 8; ++b)
+          if ((small >> b) & 1u) prod = __dmul_rn(prod, sf_one_plus_exp_m2(fabs(sm[Gm::pos(8 * k + b)])));
+        wrow[k] = (float)__ddiv_rn(1.0, prod);
+      }
+    }
+    return;
+  }
   // words 2t, 2t+1 hold indices 64 t .. 64 t + 63
   reinterpret_cast<uint2*>(words)[t] = make_uint2(s0, s1);
   reinterpret_cast<uint2*>(words + Gm::WORDS)[t] = make_uint2(m0, m1);
